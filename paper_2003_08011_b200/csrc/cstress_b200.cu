@@ -1,0 +1,733 @@
+// cstress_b200.cu -- C-ABI implementation (include/cstress_b200.h).
+//
+// Host orchestration of the B200 MSET2 path: contexts (device + streams +
+// cuSOLVER handle + workspace), device-resident models, train (selection ->
+// scale -> Gram -> eig -> pseudo-inverse -> FP32 operand packing) and the two
+// surveillance paths.  Reference citations are path:line under
+// /root/reference/proj.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "estimate_tc.cuh"
+#include "kernels_f64.cuh"
+#include "selection.cuh"
+
+using namespace csb;
+
+namespace {
+thread_local std::string g_last_error;
+
+cs_status record(cs_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <typename F>
+cs_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return CS_OK;
+  } catch (const Failure& e) {
+    return record(e.code, e.msg);
+  } catch (const std::bad_alloc&) {
+    return record(CS_ERROR, "host allocation failed");
+  } catch (const std::exception& e) {
+    return record(CS_ERROR, e.what());
+  }
+}
+
+void solver_check(cusolverStatus_t s, const char* what) {
+  if (s != CUSOLVER_STATUS_SUCCESS) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "cuSOLVER error %d in %s", static_cast<int>(s), what);
+    fail(CS_ERROR, buf);
+  }
+}
+
+int grid_for(int64_t total, int threads = 256) {
+  const int64_t b = (total + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ structs
+struct cs_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cusolverDnHandle_t solver = nullptr;
+  int sm_count = 148;
+  std::string name;
+  // workspace (grow-only)
+  DevBuf<double> wsA, wsB, wsC, wsD;
+  DevBuf<double> io_in[2], io_est[2], io_res[2];
+  DevBuf<unsigned char> wsBytes;
+};
+
+struct cs_model {
+  int device = 0;
+  int64_t n = 0, m = 0, rank = 0;
+  int kind = CS_KERNEL_INVERSE_DISTANCE;
+  double h = 0.0;
+  int precision = CS_PRECISION_FP64;
+  std::vector<int64_t> source_indices;
+  std::vector<double> spectrum_host;
+  DevBuf<double> D, Dn, scale, pinv, spectrum;
+  // FP32 tensor-core operands (precision == CS_PRECISION_FP32)
+  bool tc = false;
+  int MT = 0, K1 = 0, N2 = 0, m_tiles = 0;
+  DevBuf<float> dn_tiles, p_tiles, dd, dn32, inv_scale, scale_f;
+};
+
+namespace {
+
+void set_device(int dev) { CSB_CUDA(cudaSetDevice(dev)); }
+
+// ------------------------------------------------------------ FP64 launches
+void launch_sim_exact(cudaStream_t st, const double* A, int64_t lda, const double* B, int64_t ldb,
+                      int64_t n, int64_t p, int64_t q, int kind, double h, double* out,
+                      int64_t ldo) {
+  if (p == 0 || q == 0) return;
+  dim3 grid(ceil_div(p, kTile), ceil_div(q, kTile));
+  sim_exact_kernel<<<grid, kThreads, 0, st>>>(A, lda, B, ldb, n, p, q, kind, h, out, ldo);
+  CSB_LAUNCH_CHECK();
+}
+
+template <bool TA, bool TB>
+void launch_gemm_exact(cudaStream_t st, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       int64_t p, int64_t k, int64_t q, double* C, int64_t ldc) {
+  if (p == 0 || q == 0) return;
+  dim3 grid(ceil_div(p, kTile), ceil_div(q, kTile));
+  gemm_exact_kernel<TA, TB><<<grid, kThreads, 0, st>>>(A, lda, B, ldb, p, k, q, C, ldc);
+  CSB_LAUNCH_CHECK();
+}
+
+void check_kind(int kind) {
+  if (kind != CS_KERNEL_INVERSE_DISTANCE && kind != CS_KERNEL_GAUSSIAN)
+    fail(CS_CONFIG_ERROR, "unknown kernel kind");
+}
+
+double resolve_h(double h, int64_t n) {
+  // KernelConfig::resolved (kernels.hpp:30-34); validate() (kernels.hpp:24-27)
+  const double r = h > 0.0 ? h : std::sqrt(static_cast<double>(n));
+  if (!(r > 0.0)) fail(CS_CONFIG_ERROR, "kernel bandwidth must be > 0");
+  return r;
+}
+
+// --------------------------------------------------------------- selection
+// select_memory_vectors (mset.cpp:72-137); X is device N x n col-major.
+void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m,
+                   DevBuf<int64_t>& picked, std::vector<int64_t>& picked_host) {
+  cudaStream_t st = ctx->stream;
+  if (m < 2 * n) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "select_memory_vectors: m=%lld violates m >= 2n with n=%lld",
+                  static_cast<long long>(m), static_cast<long long>(n));
+    fail(CS_CONSTRAINT_VIOLATED, buf);
+  }
+  if (m > N) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "select_memory_vectors: m=%lld exceeds %lld training observations",
+                  static_cast<long long>(m), static_cast<long long>(N));
+    fail(CS_INSUFFICIENT_TRAINING, buf);
+  }
+  // byte workspace: hashes (2N u64), keys (2N u64), rows (2N i64), flags (N), misc
+  DevBuf<unsigned long long> h1(N), h2(N);
+  DevBuf<int64_t> r1(N), r2(N), imin(n), imax(n), npicked(1);
+  DevBuf<unsigned char> selected(N);
+  DevBuf<unsigned long long> count(1);
+  picked.resize(m);
+
+  row_hash_kernel<<<ceil_div(N, 256), 256, 0, st>>>(X, N, n, h1.get());
+  CSB_LAUNCH_CHECK();
+  size_t tmp_bytes = 0, tmp2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, h1.get(), h2.get(), static_cast<int>(N), 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp2, h1.get(), h2.get(), r1.get(), r2.get(),
+                                  static_cast<int>(N), 0, 64, st);
+  ctx->wsBytes.resize(std::max(tmp_bytes, tmp2) + 16);
+  tmp_bytes = ctx->wsBytes.count;
+  CSB_CUDA(cub::DeviceRadixSort::SortKeys(ctx->wsBytes.get(), tmp_bytes, h1.get(), h2.get(),
+                                          static_cast<int>(N), 0, 64, st));
+  CSB_CUDA(cudaMemsetAsync(count.get(), 0, sizeof(unsigned long long), st));
+  count_distinct_kernel<<<grid_for(N), 256, 0, st>>>(h2.get(), N, count.get());
+  CSB_LAUNCH_CHECK();
+  unsigned long long distinct = 0;
+  CSB_CUDA(cudaMemcpyAsync(&distinct, count.get(), sizeof distinct, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  if (static_cast<unsigned long long>(m) > distinct) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf,
+                  "select_memory_vectors: m=%lld exceeds %llu distinct training observations",
+                  static_cast<long long>(m), distinct);
+    fail(CS_INSUFFICIENT_TRAINING, buf);
+  }
+  // stage 1
+  col_extrema_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(X, N, imin.get(), imax.get());
+  CSB_LAUNCH_CHECK();
+  CSB_CUDA(cudaMemsetAsync(selected.get(), 0, N, st));
+  stage1_dedupe_kernel<<<1, 1, 0, st>>>(imin.get(), imax.get(), n, selected.get(), picked.get(),
+                                        npicked.get());
+  CSB_LAUNCH_CHECK();
+  // stage 2
+  row_norm_key_kernel<<<ceil_div(N, 256), 256, 0, st>>>(X, N, n, selected.get(), h1.get(), r1.get());
+  CSB_LAUNCH_CHECK();
+  tmp_bytes = ctx->wsBytes.count;
+  CSB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->wsBytes.get(), tmp_bytes, h1.get(), h2.get(),
+                                           r1.get(), r2.get(), static_cast<int>(N), 0, 64, st));
+  stride_pick_kernel<<<grid_for(m), 256, 0, st>>>(r2.get(), N, m, npicked.get(), picked.get());
+  CSB_LAUNCH_CHECK();
+  picked_host.resize(m);
+  CSB_CUDA(cudaMemcpyAsync(picked_host.data(), picked.get(), m * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+}
+
+// ---------------------------------------------------------- eigensolver
+// symmetric_eig (mset.cpp:57-70): precondition check, then cuSOLVER syevd
+// (FP64, ascending eigenvalues, orthonormal eigenvectors) in place on V.
+void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
+  cudaStream_t st = ctx->stream;
+  if (m == 0) return;
+  DevBuf<unsigned long long> stats(2);
+  CSB_CUDA(cudaMemsetAsync(stats.get(), 0, 2 * sizeof(unsigned long long), st));
+  symmetry_stats_kernel<<<grid_for(m * m), 256, 0, st>>>(G, m, stats.get());
+  CSB_LAUNCH_CHECK();
+  unsigned long long hs[2];
+  CSB_CUDA(cudaMemcpyAsync(hs, stats.get(), sizeof hs, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  double mag, asym;
+  std::memcpy(&mag, &hs[0], 8);
+  std::memcpy(&asym, &hs[1], 8);
+  if (asym > 1e-9 * std::max(mag, 1.0)) fail(CS_SHAPE_ERROR, "symmetric_eig: matrix is not symmetric to 1e-9");
+  if (V != G) CSB_CUDA(cudaMemcpyAsync(V, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  solver_check(cusolverDnSetStream(ctx->solver, st), "SetStream");
+  int lwork = 0;
+  solver_check(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR,
+                                           CUBLAS_FILL_MODE_LOWER, static_cast<int>(m), V,
+                                           static_cast<int>(m), w, &lwork),
+               "Dsyevd_bufferSize");
+  DevBuf<double> work(static_cast<size_t>(lwork) + 1);
+  DevBuf<int> info(1);
+  solver_check(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                static_cast<int>(m), V, static_cast<int>(m), w, work.get(), lwork,
+                                info.get()),
+               "Dsyevd");
+  int hinfo = 0;
+  CSB_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof hinfo, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  if (hinfo != 0) fail(CS_EIG_FAILURE, "symmetric_eig: eigensolver did not converge");
+}
+
+// ------------------------------------------------------ FP32 operand packing
+void choose_tc_shape(cs_model* M) {
+  M->K1 = static_cast<int>((M->n + 7) / 8 * 8);
+  M->N2 = static_cast<int>((M->n + 15) / 16 * 16);
+  M->MT = 0;
+  const int cand[4] = {128, 64, 32, 16};
+  for (int MT : cand) {
+    const int cols = M->N2 + 2 * M->K1 + 3 * MT;
+    const size_t stage = static_cast<size_t>(2) * MT * M->K1 * 4 + static_cast<size_t>(2) * M->N2 * MT * 4;
+    const size_t smem = 2 * stage + 256;
+    if (cols <= kTmemCols && smem <= 227 * 1024) {
+      M->MT = MT;
+      break;
+    }
+  }
+  M->tc = M->MT > 0;
+  if (M->tc) M->m_tiles = static_cast<int>((M->m + M->MT - 1) / M->MT);
+}
+
+void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
+  cudaStream_t st = ctx->stream;
+  choose_tc_shape(M);
+  if (!M->tc) return;
+  const int n = static_cast<int>(M->n), m = static_cast<int>(M->m);
+  // P = D_norm * G+  (n x m), FP64, once per model
+  DevBuf<double> P(static_cast<size_t>(n) * m);
+  launch_gemm_exact<false, false>(st, M->Dn.get(), n, M->pinv.get(), m, n, m, m, P.get(), n);
+  const int m_pad = M->m_tiles * M->MT;
+  M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
+  M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
+  M->dd.resize(m_pad);
+  M->dn32.resize(static_cast<size_t>(n) * m);
+  M->inv_scale.resize(n);
+  M->scale_f.resize(n);
+  pack_dn_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->K1), 256, 0, st>>>(
+      M->Dn.get(), n, m, M->MT, M->K1, M->m_tiles, M->dn_tiles.get());
+  CSB_LAUNCH_CHECK();
+  pack_p_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->N2), 256, 0, st>>>(
+      P.get(), n, m, M->MT, M->N2, M->m_tiles, M->p_tiles.get());
+  CSB_LAUNCH_CHECK();
+  pack_aux_kernel<<<grid_for(std::max<int64_t>(m_pad, static_cast<int64_t>(n) * m)), 256, 0, st>>>(
+      M->Dn.get(), M->scale.get(), n, m, m_pad, M->dd.get(), M->dn32.get(), M->inv_scale.get(),
+      M->scale_f.get());
+  CSB_LAUNCH_CHECK();
+  CSB_CUDA(cudaStreamSynchronize(st));  // P is freed on return
+}
+
+// ----------------------------------------------------------------- train
+cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m, int kind,
+                       double bandwidth, int precision) {
+  check_kind(kind);
+  if (precision != CS_PRECISION_FP64 && precision != CS_PRECISION_FP32)
+    fail(CS_CONFIG_ERROR, "unknown precision");
+  cudaStream_t st = ctx->stream;
+  std::unique_ptr<cs_model> M(new cs_model);
+  M->device = ctx->device;
+  M->n = n;
+  M->m = m;
+  M->kind = kind;
+  M->precision = precision;
+  DevBuf<int64_t> picked;
+  select_device(ctx, X, N, n, m, picked, M->source_indices);  // mset.cpp:142
+  M->h = resolve_h(bandwidth, n);                            // mset.cpp:143-144
+  M->D.resize(n * m);
+  gather_memory_kernel<<<grid_for(n * m), 256, 0, st>>>(X, N, n, picked.get(), m, M->D.get());
+  CSB_LAUNCH_CHECK();
+  M->scale.resize(n);                                        // mset.cpp:145
+  scale_seq_kernel<<<ceil_div(n, 32), 128, 0, st>>>(X, N, n, M->scale.get());
+  CSB_LAUNCH_CHECK();
+  M->Dn.resize(n * m);                                       // mset.cpp:147-149
+  div_rows_kernel<<<grid_for(n * m), 256, 0, st>>>(M->D.get(), M->scale.get(), n, m, M->Dn.get());
+  CSB_LAUNCH_CHECK();
+  DevBuf<double> gram(m * m), V(m * m);                      // mset.cpp:151-152
+  launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, kind, M->h, gram.get(), m);
+  M->spectrum.resize(m);                                     // mset.cpp:153-154
+  eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get());
+  M->spectrum_host.resize(m);
+  CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  const double cutoff = 1e-10 * M->spectrum_host[m - 1];    // mset.cpp:156-163
+  int64_t rank = 0;
+  for (int64_t i = 0; i < m; ++i)
+    if (M->spectrum_host[i] > cutoff) ++rank;
+  if (rank == 0) fail(CS_DEGENERATE_MODEL, "train: all Gram eigenvalues below cutoff");
+  M->rank = rank;
+  DevBuf<double> W(m * rank);                                // mset.cpp:165-170
+  whiten_kernel<<<grid_for(m * rank), 256, 0, st>>>(V.get(), M->spectrum.get(), m, rank, W.get());
+  CSB_LAUNCH_CHECK();
+  M->pinv.resize(m * m);
+  launch_gemm_exact<false, true>(st, W.get(), m, W.get(), m, m, rank, m, M->pinv.get(), m);
+  if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
+  CSB_CUDA(cudaStreamSynchronize(st));
+  return M.release();
+}
+
+// ------------------------------------------------------------- estimate
+void check_model_shape(const cs_model* M, int64_t n) {
+  if (n != M->n) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf,
+                  "estimate: observation signal count %lld does not match model signal count %lld",
+                  static_cast<long long>(n), static_cast<long long>(M->n));
+    fail(CS_SHAPE_ERROR, buf);
+  }
+  if (M->rank < 1) fail(CS_DEGENERATE_MODEL, "estimate: model rank is 0");
+}
+
+// FP64, reference association, exact order (mset.cpp:186-197).  Device
+// buffers; processes observations in chunks of the S/W workspace.
+void estimate_fp64_device(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const double* obs,
+                          int64_t N, int64_t ld, double* est, double* resid) {
+  const int64_t n = M->n, m = M->m;
+  const int64_t budget = (int64_t{1} << 28);  // doubles per m x Nc workspace
+  const int64_t Nc = std::max<int64_t>(1, std::min<int64_t>(N, budget / std::max<int64_t>(m, 1)));
+  ctx->wsA.resize(n * Nc);
+  ctx->wsB.resize(m * Nc);
+  ctx->wsC.resize(m * Nc);
+  ctx->wsD.resize(n * Nc);
+  for (int64_t t0 = 0; t0 < N; t0 += Nc) {
+    const int64_t nc = std::min(Nc, N - t0);
+    dim3 tg(ceil_div(nc, 32), ceil_div(n, 32)), tb(32, 8);
+    transpose_div_kernel<<<tg, tb, 0, st>>>(obs, ld, t0, nc, n, M->scale.get(), ctx->wsA.get());
+    CSB_LAUNCH_CHECK();
+    launch_sim_exact(st, M->Dn.get(), n, ctx->wsA.get(), n, n, m, nc, M->kind, M->h, ctx->wsB.get(), m);
+    launch_gemm_exact<false, false>(st, M->pinv.get(), m, ctx->wsB.get(), m, m, m, nc, ctx->wsC.get(), m);
+    launch_gemm_exact<false, false>(st, M->Dn.get(), n, ctx->wsC.get(), m, n, m, nc, ctx->wsD.get(), n);
+    finish_estimate_kernel<<<tg, tb, 0, st>>>(ctx->wsD.get(), nc, n, M->scale.get(), obs, ld, t0,
+                                              est, resid);
+    CSB_LAUNCH_CHECK();
+  }
+}
+
+template <typename IO>
+void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, int64_t N,
+               int64_t ld, IO* est, IO* resid) {
+  if (N == 0) return;
+  TcParams p{};
+  p.obs = obs;
+  p.N = N;
+  p.ld = ld;
+  p.n = static_cast<int>(M->n);
+  p.K1 = M->K1;
+  p.N2 = M->N2;
+  p.m = static_cast<int>(M->m);
+  p.m_tiles = M->m_tiles;
+  p.dn_tiles = M->dn_tiles.get();
+  p.p_tiles = M->p_tiles.get();
+  p.dd = M->dd.get();
+  p.dn32 = M->dn32.get();
+  p.inv_scale = M->inv_scale.get();
+  p.scale_f = M->scale_f.get();
+  p.scale_d = M->scale.get();
+  p.kind = M->kind;
+  p.inv_h = static_cast<float>(1.0 / M->h);
+  p.g_coef = static_cast<float>(1.4426950408889634 / (2.0 * M->h * M->h));
+  p.tau = 1.0f / 128.0f;
+  p.est = est;
+  p.resid = resid;
+  p.dn_stage_bytes = static_cast<uint32_t>(2 * M->MT * M->K1 * 4);
+  p.p_stage_bytes = static_cast<uint32_t>(2 * M->N2 * M->MT * 4);
+  const size_t smem = 2 * (static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes) + 256;
+  const int tiles = static_cast<int>((N + kObsTile - 1) / kObsTile);
+  const int grid = std::min(tiles, ctx->sm_count);
+  auto go = [&](auto kernel) {
+    CSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    kernel<<<grid, kTcThreads, smem, st>>>(p);
+    CSB_LAUNCH_CHECK();
+  };
+  switch (M->MT) {
+    case 128: go(mset_estimate_tc_kernel<128, IO>); break;
+    case 64: go(mset_estimate_tc_kernel<64, IO>); break;
+    case 32: go(mset_estimate_tc_kernel<32, IO>); break;
+    case 16: go(mset_estimate_tc_kernel<16, IO>); break;
+    default: fail(CS_ERROR, "internal: bad tensor-core tile width");
+  }
+}
+
+void estimate_device_any(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const void* obs,
+                         int dtype, int64_t N, int64_t ld, void* est, void* resid) {
+  if (M->precision == CS_PRECISION_FP32 && M->tc) {
+    if (dtype == CS_DTYPE_F32)
+      launch_tc<float>(ctx, st, M, static_cast<const float*>(obs), N, ld, static_cast<float*>(est),
+                       static_cast<float*>(resid));
+    else
+      launch_tc<double>(ctx, st, M, static_cast<const double*>(obs), N, ld,
+                        static_cast<double*>(est), static_cast<double*>(resid));
+    return;
+  }
+  // FP64 path (also serves FP32 models whose n exceeds the fused kernel's
+  // TMEM budget -- see DESIGN.md "large-n surveillance").
+  if (dtype != CS_DTYPE_F64) fail(CS_CONFIG_ERROR, "FP64 surveillance requires FP64 device I/O");
+  estimate_fp64_device(ctx, st, M, static_cast<const double*>(obs), N, ld,
+                       static_cast<double*>(est), static_cast<double*>(resid));
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+const char* cs_last_error(void) { return g_last_error.c_str(); }
+
+// error channel for the host-side data feed (synth.cpp)
+cs_status cs__set_error(cs_status code, const char* msg) {
+  g_last_error = msg ? msg : "";
+  return code;
+}
+const char* cs_version(void) { return "cstress-b200 0.1.0 (sm_100a)"; }
+
+cs_status cs_ctx_create(int device, cs_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(CS_CONFIG_ERROR, "cs_ctx_create: null output");
+    int count = 0;
+    CSB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) fail(CS_CONFIG_ERROR, "cs_ctx_create: no such device");
+    set_device(device);
+    std::unique_ptr<cs_ctx> c(new cs_ctx);
+    c->device = device;
+    cudaDeviceProp prop{};
+    CSB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(CS_ERROR, std::string("cs_ctx_create: sm_100a device required, found ") + prop.name);
+    c->sm_count = prop.multiProcessorCount;
+    c->name = prop.name;
+    CSB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking));
+    CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
+    c->stream = c->own;
+    solver_check(cusolverDnCreate(&c->solver), "cusolverDnCreate");
+    *out = c.release();
+  });
+}
+
+cs_status cs_ctx_destroy(cs_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    set_device(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1]})
+      if (s) cudaStreamDestroy(s);
+    delete ctx;
+  });
+}
+
+cs_status cs_ctx_set_stream(cs_ctx* ctx, void* stream) {
+  return guarded([&] {
+    if (!ctx) fail(CS_CONFIG_ERROR, "null context");
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  });
+}
+
+cs_status cs_ctx_synchronize(cs_ctx* ctx) {
+  return guarded([&] {
+    set_device(ctx->device);
+    CSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+cs_status cs_ctx_describe(cs_ctx* ctx, char* buf, size_t buflen) {
+  return guarded([&] {
+    std::snprintf(buf, buflen,
+                  "%s, %d SMs; FP64 exact-order SIMT (train, reference-association "
+                  "surveillance); tcgen05 3xTF32 fused surveillance; cuSOLVER syevd",
+                  ctx->name.c_str(), ctx->sm_count);
+  });
+}
+
+cs_status cs_sim_matrix(cs_ctx* ctx, const double* A, const double* B, int64_t n, int64_t p,
+                        int64_t q, int kind, double bandwidth, double* out) {
+  return guarded([&] {
+    check_kind(kind);
+    set_device(ctx->device);
+    const double h = resolve_h(bandwidth, n);
+    if (p == 0 || q == 0) return;
+    DevBuf<double> dA(n * p + 1), dB(n * q + 1), dO(p * q);
+    cudaStream_t st = ctx->stream;
+    CSB_CUDA(cudaMemcpyAsync(dA.get(), A, n * p * sizeof(double), cudaMemcpyHostToDevice, st));
+    CSB_CUDA(cudaMemcpyAsync(dB.get(), B, n * q * sizeof(double), cudaMemcpyHostToDevice, st));
+    launch_sim_exact(st, dA.get(), n, dB.get(), n, n, p, q, kind, h, dO.get(), p);
+    CSB_CUDA(cudaMemcpyAsync(out, dO.get(), p * q * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+cs_status cs_matmul(cs_ctx* ctx, const double* A, const double* B, int64_t p, int64_t k, int64_t q,
+                    double* out) {
+  return guarded([&] {
+    set_device(ctx->device);
+    if (p == 0 || q == 0) return;
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> dA(p * k + 1), dB(k * q + 1), dO(p * q);
+    CSB_CUDA(cudaMemcpyAsync(dA.get(), A, p * k * sizeof(double), cudaMemcpyHostToDevice, st));
+    CSB_CUDA(cudaMemcpyAsync(dB.get(), B, k * q * sizeof(double), cudaMemcpyHostToDevice, st));
+    launch_gemm_exact<false, false>(st, dA.get(), p, dB.get(), k, p, k, q, dO.get(), p);
+    CSB_CUDA(cudaMemcpyAsync(out, dO.get(), p * q * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+cs_status cs_batched_solve(cs_ctx* ctx, const double* G, const double* S, int64_t m, int64_t q,
+                           double* out) {
+  // backends.cpp:288-293: batched_solve(G+, S) == matmul(G+, S)
+  return cs_matmul(ctx, G, S, m, m, q, out);
+}
+
+cs_status cs_symmetric_eig(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
+  return guarded([&] {
+    set_device(ctx->device);
+    if (m == 0) return;
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> dG(m * m), dV(m * m), dw(m);
+    CSB_CUDA(cudaMemcpyAsync(dG.get(), G, m * m * sizeof(double), cudaMemcpyHostToDevice, st));
+    eig_device(ctx, dG.get(), m, dw.get(), dV.get());
+    CSB_CUDA(cudaMemcpyAsync(w, dw.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaMemcpyAsync(V, dV.get(), m * m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+cs_status cs_select_memory_vectors(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m,
+                                   int64_t* idx, double* D) {
+  return guarded([&] {
+    set_device(ctx->device);
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> dX(N * n + 1);
+    CSB_CUDA(cudaMemcpyAsync(dX.get(), X, N * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    DevBuf<int64_t> picked;
+    std::vector<int64_t> host;
+    select_device(ctx, dX.get(), N, n, m, picked, host);
+    std::memcpy(idx, host.data(), m * sizeof(int64_t));
+    if (D) {
+      DevBuf<double> dD(n * m);
+      gather_memory_kernel<<<grid_for(n * m), 256, 0, st>>>(dX.get(), N, n, picked.get(), m, dD.get());
+      CSB_LAUNCH_CHECK();
+      CSB_CUDA(cudaMemcpyAsync(D, dD.get(), n * m * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CSB_CUDA(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+cs_status cs_mset_train_device(cs_ctx* ctx, const double* dX, int64_t N, int64_t n, int64_t m,
+                               int kind, double bandwidth, int precision, cs_model** out) {
+  return guarded([&] {
+    if (!out) fail(CS_CONFIG_ERROR, "cs_mset_train: null output");
+    set_device(ctx->device);
+    *out = train_device(ctx, dX, N, n, m, kind, bandwidth, precision);
+  });
+}
+
+cs_status cs_mset_train(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m, int kind,
+                        double bandwidth, int precision, cs_model** out) {
+  return guarded([&] {
+    if (!out) fail(CS_CONFIG_ERROR, "cs_mset_train: null output");
+    set_device(ctx->device);
+    DevBuf<double> dX(N * n + 1);
+    CSB_CUDA(cudaMemcpyAsync(dX.get(), X, N * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    *out = train_device(ctx, dX.get(), N, n, m, kind, bandwidth, precision);
+  });
+}
+
+cs_status cs_mset_estimate_device(cs_ctx* ctx, const cs_model* M, const void* obs, int dtype,
+                                  int64_t N, int64_t n, int64_t ld, void* est, void* resid) {
+  return guarded([&] {
+    if (!M) fail(CS_CONFIG_ERROR, "model was not trained by algorithm mset2");
+    set_device(ctx->device);
+    check_model_shape(M, n);
+    if (ld < N) fail(CS_SHAPE_ERROR, "estimate: leading dimension smaller than observation count");
+    estimate_device_any(ctx, ctx->stream, M, obs, dtype, N, ld, est, resid);
+  });
+}
+
+// Host FP64 in/out: chunks alternate over two streams, each running
+// H2D -> kernel -> D2H, so copies in both directions overlap compute.
+cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, int64_t N,
+                           int64_t n, double* est, double* resid) {
+  return guarded([&] {
+    if (!M) fail(CS_CONFIG_ERROR, "model was not trained by algorithm mset2");
+    set_device(ctx->device);
+    check_model_shape(M, n);
+    if (N == 0) return;
+    const bool tc = M->precision == CS_PRECISION_FP32 && M->tc;
+    // chunk: a multiple of the 128-observation tile, ~32 MB of input
+    int64_t Nc = std::max<int64_t>(kObsTile, (int64_t{1} << 22) / std::max<int64_t>(n, 1));
+    Nc = (Nc + kObsTile - 1) / kObsTile * kObsTile;
+    if (!tc) Nc = std::max<int64_t>(1, std::min<int64_t>(Nc, (int64_t{1} << 27) / std::max<int64_t>(M->m, 1)));
+    Nc = std::min(Nc, N);
+    cudaEvent_t start;
+    CSB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventRecord(start, ctx->stream));
+    for (int b = 0; b < 2; ++b) {
+      ctx->io_in[b].resize(Nc * n);
+      ctx->io_est[b].resize(Nc * n);
+      ctx->io_res[b].resize(Nc * n);
+      CSB_CUDA(cudaStreamWaitEvent(ctx->aux[b], start, 0));
+    }
+    int64_t chunk = 0;
+    for (int64_t t0 = 0; t0 < N; t0 += Nc, ++chunk) {
+      const int b = static_cast<int>(chunk & 1);
+      cudaStream_t st = ctx->aux[b];
+      const int64_t nc = std::min(Nc, N - t0);
+      CSB_CUDA(cudaMemcpy2DAsync(ctx->io_in[b].get(), nc * sizeof(double), obs + t0, N * sizeof(double),
+                                 nc * sizeof(double), n, cudaMemcpyHostToDevice, st));
+      double* de = est ? ctx->io_est[b].get() : nullptr;
+      double* dr = resid ? ctx->io_res[b].get() : nullptr;
+      if (tc) {
+        launch_tc<double>(ctx, st, M, ctx->io_in[b].get(), nc, nc, de, dr);
+      } else {
+        estimate_fp64_device(ctx, st, M, ctx->io_in[b].get(), nc, nc, de, dr);
+      }
+      if (est)
+        CSB_CUDA(cudaMemcpy2DAsync(est + t0, N * sizeof(double), de, nc * sizeof(double),
+                                   nc * sizeof(double), n, cudaMemcpyDeviceToHost, st));
+      if (resid)
+        CSB_CUDA(cudaMemcpy2DAsync(resid + t0, N * sizeof(double), dr, nc * sizeof(double),
+                                   nc * sizeof(double), n, cudaMemcpyDeviceToHost, st));
+      if (!tc) CSB_CUDA(cudaStreamSynchronize(st));  // FP64 path shares one workspace
+    }
+    CSB_CUDA(cudaStreamSynchronize(ctx->aux[0]));
+    CSB_CUDA(cudaStreamSynchronize(ctx->aux[1]));
+    cudaEventDestroy(start);
+  });
+}
+
+cs_status cs_model_info(const cs_model* M, int64_t* n, int64_t* m, int64_t* rank, int* kind,
+                        double* h, int* precision) {
+  return guarded([&] {
+    if (!M) fail(CS_CONFIG_ERROR, "null model");
+    if (n) *n = M->n;
+    if (m) *m = M->m;
+    if (rank) *rank = M->rank;
+    if (kind) *kind = M->kind;
+    if (h) *h = M->h;
+    if (precision) *precision = M->precision;
+  });
+}
+
+cs_status cs_model_export(const cs_model* M, int64_t* idx, double* D, double* pinv, double* spectrum,
+                          double* scale) {
+  return guarded([&] {
+    if (!M) fail(CS_CONFIG_ERROR, "null model");
+    set_device(M->device);
+    const int64_t n = M->n, m = M->m;
+    if (idx) std::memcpy(idx, M->source_indices.data(), m * sizeof(int64_t));
+    if (D) CSB_CUDA(cudaMemcpy(D, M->D.get(), n * m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (pinv) CSB_CUDA(cudaMemcpy(pinv, M->pinv.get(), m * m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (spectrum) std::memcpy(spectrum, M->spectrum_host.data(), m * sizeof(double));
+    if (scale) CSB_CUDA(cudaMemcpy(scale, M->scale.get(), n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+cs_status cs_model_import(cs_ctx* ctx, int64_t n, int64_t m, int kind, double bandwidth, int64_t rank,
+                          const int64_t* idx, const double* D, const double* pinv,
+                          const double* spectrum, const double* scale, int precision,
+                          cs_model** out) {
+  return guarded([&] {
+    check_kind(kind);
+    if (!out || !D || !pinv || !scale) fail(CS_CONFIG_ERROR, "cs_model_import: null argument");
+    set_device(ctx->device);
+    cudaStream_t st = ctx->stream;
+    std::unique_ptr<cs_model> M(new cs_model);
+    M->device = ctx->device;
+    M->n = n;
+    M->m = m;
+    M->rank = rank;
+    M->kind = kind;
+    M->h = resolve_h(bandwidth, n);
+    M->precision = precision;
+    M->source_indices.assign(idx ? idx : nullptr, idx ? idx + m : nullptr);
+    if (!idx) M->source_indices.assign(m, -1);
+    M->spectrum_host.assign(spectrum ? spectrum : nullptr, spectrum ? spectrum + m : nullptr);
+    if (!spectrum) M->spectrum_host.assign(m, 0.0);
+    M->D.resize(n * m);
+    M->Dn.resize(n * m);
+    M->scale.resize(n);
+    M->pinv.resize(m * m);
+    M->spectrum.resize(m);
+    CSB_CUDA(cudaMemcpyAsync(M->D.get(), D, n * m * sizeof(double), cudaMemcpyHostToDevice, st));
+    CSB_CUDA(cudaMemcpyAsync(M->scale.get(), scale, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CSB_CUDA(cudaMemcpyAsync(M->pinv.get(), pinv, m * m * sizeof(double), cudaMemcpyHostToDevice, st));
+    CSB_CUDA(cudaMemcpyAsync(M->spectrum.get(), M->spectrum_host.data(), m * sizeof(double),
+                             cudaMemcpyHostToDevice, st));
+    // load_model rebuilds memory_normalized (mset.cpp:306-308)
+    div_rows_kernel<<<grid_for(n * m), 256, 0, st>>>(M->D.get(), M->scale.get(), n, m, M->Dn.get());
+    CSB_LAUNCH_CHECK();
+    if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
+    CSB_CUDA(cudaStreamSynchronize(st));
+    *out = M.release();
+  });
+}
+
+cs_status cs_model_destroy(cs_model* M) {
+  return guarded([&] {
+    if (!M) return;
+    cudaSetDevice(M->device);
+    delete M;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,373 @@
+"""Host-side mirror of the reference MSET2 interface for the B200 backend.
+
+Mirrors /root/reference/proj/include/containerstress/{kernels,backends,mset}.hpp:
+same names, argument meaning and error behaviour, so the parity tests read
+like the reference's own tests.  Every compute call goes through the C-ABI
+(include/cstress_b200.h) into libcstress_b200.so; nothing here computes on
+the CPU.
+
+Layouts follow the reference (types.hpp:7-15): column-major FP64;
+signal matrices are observations x signals; memory matrices are
+signals x memory vectors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import re
+import threading
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, f64, ptr_d, ptr_i64
+from .errors import ConfigError, ShapeError
+
+# ------------------------------------------------------------------ kernels
+class KernelKind(IntEnum):
+    """kernels.hpp:12"""
+    inverse_distance = 0
+    gaussian = 1
+
+
+@dataclass
+class KernelConfig:
+    """kernels.hpp:20-35.  bandwidth None -> sqrt(n_signals) at training."""
+    kind: KernelKind = KernelKind.inverse_distance
+    bandwidth: Optional[float] = None
+
+    def validate(self) -> None:
+        if self.bandwidth is not None and not self.bandwidth > 0.0:
+            raise ConfigError("kernel bandwidth must be > 0")
+
+    def resolved(self, n_signals: int) -> "KernelConfig":
+        return KernelConfig(self.kind, self.bandwidth if self.bandwidth is not None
+                            else math.sqrt(float(n_signals)))
+
+    def _h(self) -> float:
+        self.validate()
+        return float(self.bandwidth) if self.bandwidth is not None else 0.0
+
+
+PRECISIONS = {"fp64": 0, "fp32": 1}
+
+
+# ----------------------------------------------------------------- backends
+@dataclass(frozen=True)
+class BackendId:
+    """backends.hpp:14-33 plus the B200 kind this framework implements.
+
+    ``precision`` selects the surveillance arithmetic: ``fp64`` reproduces
+    the reference's association and summation order bit-for-bit;
+    ``fp32`` runs the fused tcgen05 3xTF32 kernel (tolerance 1e-3).
+    """
+    kind: str = "b200"
+    device: int = 0
+    precision: str = "fp64"
+
+    def validate(self) -> None:
+        if self.kind != "b200":
+            raise ConfigError(f"unknown backend id: {self.kind}")
+        if self.device < 0:
+            raise ConfigError("backend device must be >= 0")
+        if self.precision not in PRECISIONS:
+            raise ConfigError(f"unknown precision: {self.precision}")
+
+    def label(self) -> str:
+        return f"b200[device={self.device}/precision={self.precision}]"
+
+    @staticmethod
+    def parse(token: str) -> "BackendId":
+        if token == "b200":
+            return BackendId()
+        m = re.fullmatch(r"b200\[device=(\d+)/precision=(fp32|fp64)\]", token)
+        if m:
+            return BackendId("b200", int(m.group(1)), m.group(2))
+        raise ConfigError("unknown backend id: " + token)
+
+
+# ----------------------------------------------------------------- contexts
+class Context:
+    """One cs_ctx: device + stream + cuSOLVER handle + workspace."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        check(_lib.lib().cs_ctx_create(device, C.byref(h)))
+        self.handle = h
+
+    def describe(self) -> str:
+        buf = C.create_string_buffer(512)
+        check(_lib.lib().cs_ctx_describe(self.handle, buf, 512))
+        return buf.value.decode()
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        check(_lib.lib().cs_ctx_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self) -> None:
+        check(_lib.lib().cs_ctx_synchronize(self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().cs_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_contexts: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def context(device: int = 0) -> Context:
+    key = (threading.get_ident(), device)
+    with _ctx_lock:
+        if key not in _contexts:
+            _contexts[key] = Context(device)
+        return _contexts[key]
+
+
+def _ctx(backend: BackendId) -> Context:
+    backend.validate()
+    return context(backend.device)
+
+
+@dataclass
+class BackendCapabilities:
+    """backends.hpp:35-41"""
+    id: BackendId
+    deterministic_summation: bool = True
+    description: str = ""
+
+
+def capabilities(backend: BackendId) -> BackendCapabilities:
+    return BackendCapabilities(backend, True, _ctx(backend).describe())
+
+
+# ------------------------------------------------------------ per-op entries
+def sim_matrix(A, B, cfg: KernelConfig = KernelConfig(), backend: BackendId = BackendId()):
+    """backends.hpp:43-58 -- entry (i, j) = kernel(col i of A, col j of B)."""
+    A, B = f64(A), f64(B)
+    if A.shape[0] != B.shape[0]:
+        raise ShapeError(f"sim_matrix: row counts differ ({A.shape[0]} vs {B.shape[0]})")
+    n, p = A.shape
+    q = B.shape[1]
+    out = np.empty((p, q), order="F")
+    check(_lib.lib().cs_sim_matrix(_ctx(backend).handle, ptr_d(A), ptr_d(B), n, p, q,
+                                   int(cfg.kind), cfg._h(), ptr_d(out)))
+    return out
+
+
+similarity_matrix = sim_matrix  # mset.hpp:65-70
+
+
+def matmul(A, B, backend: BackendId = BackendId()):
+    """backends.hpp:60-61"""
+    A, B = f64(A), f64(B)
+    if A.shape[1] != B.shape[0]:
+        raise ShapeError(f"matmul: inner dimensions differ ({A.shape[1]} vs {B.shape[0]})")
+    out = np.empty((A.shape[0], B.shape[1]), order="F")
+    check(_lib.lib().cs_matmul(_ctx(backend).handle, ptr_d(A), ptr_d(B), A.shape[0], A.shape[1],
+                               B.shape[1], ptr_d(out)))
+    return out
+
+
+def batched_solve(G_pinv, S, backend: BackendId = BackendId()):
+    """backends.hpp:63-65 (== matmul(G_pinv, S))"""
+    G_pinv, S = f64(G_pinv), f64(S)
+    if G_pinv.shape[1] != S.shape[0]:
+        raise ShapeError("batched_solve: G_pinv columns must match S rows")
+    out = np.empty((G_pinv.shape[0], S.shape[1]), order="F")
+    check(_lib.lib().cs_batched_solve(_ctx(backend).handle, ptr_d(G_pinv), ptr_d(S),
+                                      G_pinv.shape[0], S.shape[1], ptr_d(out)))
+    return out
+
+
+@dataclass
+class SymmetricEig:
+    eigenvalues: np.ndarray
+    eigenvectors: np.ndarray
+
+
+def symmetric_eig(G, backend: BackendId = BackendId()) -> SymmetricEig:
+    """mset.hpp:34-38"""
+    G = f64(G)
+    if G.ndim != 2 or G.shape[0] != G.shape[1]:
+        raise ShapeError("symmetric_eig: matrix is not square")
+    m = G.shape[0]
+    w = np.empty(m)
+    V = np.empty((m, m), order="F")
+    check(_lib.lib().cs_symmetric_eig(_ctx(backend).handle, ptr_d(G), m, ptr_d(w), ptr_d(V)))
+    return SymmetricEig(w, V)
+
+
+@dataclass
+class MemoryMatrix:
+    """mset.hpp:21-27"""
+    D: np.ndarray
+    source_indices: list
+
+    def n_signals(self):
+        return self.D.shape[0]
+
+    def n_memory(self):
+        return self.D.shape[1]
+
+
+def _signal_data(x):
+    return f64(getattr(x, "data", x))
+
+
+def select_memory_vectors(training, m: int, backend: BackendId = BackendId()) -> MemoryMatrix:
+    """mset.hpp:40-43 / mset.cpp:72-137 (bit-exact indices)."""
+    X = _signal_data(training)
+    N, n = X.shape
+    idx = np.empty(m, dtype=np.int64)
+    D = np.empty((n, m), order="F")
+    check(_lib.lib().cs_select_memory_vectors(_ctx(backend).handle, ptr_d(X), N, n, m,
+                                              ptr_i64(idx), ptr_d(D)))
+    return MemoryMatrix(D, idx.tolist())
+
+
+# ------------------------------------------------------------ train/estimate
+class TrainedModel:
+    """Device-resident TrainedModel (mset.hpp:46-57); immutable after training."""
+
+    def __init__(self, handle: C.c_void_p, backend: BackendId):
+        self.handle = handle
+        self.backend = backend
+        n, m, r, kind, prec = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+        h = C.c_double()
+        check(_lib.lib().cs_model_info(handle, C.byref(n), C.byref(m), C.byref(r), C.byref(kind),
+                                       C.byref(h), C.byref(prec)))
+        self._n, self._m, self.rank = n.value, m.value, r.value
+        self.kernel = KernelConfig(KernelKind(kind.value), h.value)
+        self.precision = prec.value
+        self._export = None
+
+    def n_signals(self):
+        return self._n
+
+    def n_memory(self):
+        return self._m
+
+    def export(self) -> dict:
+        if self._export is None:
+            n, m = self._n, self._m
+            idx = np.empty(m, dtype=np.int64)
+            D = np.empty((n, m), order="F")
+            pinv = np.empty((m, m), order="F")
+            spec = np.empty(m)
+            scale = np.empty(n)
+            check(_lib.lib().cs_model_export(self.handle, ptr_i64(idx), ptr_d(D), ptr_d(pinv),
+                                             ptr_d(spec), ptr_d(scale)))
+            self._export = dict(source_indices=idx, D=D, gram_pinv=pinv, eigen_spectrum=spec,
+                                signal_scale=scale)
+        return self._export
+
+    @property
+    def memory(self) -> MemoryMatrix:
+        e = self.export()
+        return MemoryMatrix(e["D"], e["source_indices"].tolist())
+
+    @property
+    def gram_pinv(self):
+        return self.export()["gram_pinv"]
+
+    @property
+    def eigen_spectrum(self):
+        return self.export()["eigen_spectrum"]
+
+    @property
+    def signal_scale(self):
+        return self.export()["signal_scale"]
+
+    @property
+    def memory_normalized(self):
+        e = self.export()
+        return e["D"] / e["signal_scale"][:, None]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().cs_model_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def train(training, m: int, cfg: KernelConfig = KernelConfig(),
+          backend: BackendId = BackendId()) -> TrainedModel:
+    """mset.hpp:72-77 / mset.cpp:139-172."""
+    X = _signal_data(training)
+    N, n = X.shape
+    h = C.c_void_p()
+    check(_lib.lib().cs_mset_train(_ctx(backend).handle, ptr_d(X), N, n, m, int(cfg.kind),
+                                   cfg._h(), PRECISIONS[backend.precision], C.byref(h)))
+    return TrainedModel(h, backend)
+
+
+def import_model(D, signal_scale, gram_pinv, rank, cfg: KernelConfig,
+                 backend: BackendId = BackendId(), source_indices=None,
+                 eigen_spectrum=None) -> TrainedModel:
+    """Host TrainedModel -> device (the load_model path, mset.cpp:269-310)."""
+    D, sc, pv = f64(D), f64(signal_scale), f64(gram_pinv)
+    n, m = D.shape
+    idx = None if source_indices is None else np.ascontiguousarray(source_indices, dtype=np.int64)
+    sp = None if eigen_spectrum is None else f64(eigen_spectrum)
+    h = C.c_void_p()
+    check(_lib.lib().cs_model_import(
+        _ctx(backend).handle, n, m, int(cfg.kind), cfg._h(), int(rank),
+        ptr_i64(idx) if idx is not None else None, ptr_d(D), ptr_d(pv),
+        ptr_d(sp) if sp is not None else None, ptr_d(sc), PRECISIONS[backend.precision],
+        C.byref(h)))
+    return TrainedModel(h, backend)
+
+
+@dataclass
+class EstimationResult:
+    """mset.hpp:59-62"""
+    estimates: np.ndarray
+    residuals: np.ndarray
+
+
+def estimate(model: TrainedModel, observations, backend: Optional[BackendId] = None
+             ) -> EstimationResult:
+    """mset.hpp:79-82 / mset.cpp:174-199 -- host FP64 in and out."""
+    backend = backend or model.backend
+    obs = _signal_data(observations)
+    N, n = obs.shape
+    est = np.empty((N, n), order="F")
+    res = np.empty((N, n), order="F")
+    check(_lib.lib().cs_mset_estimate(_ctx(backend).handle, model.handle, ptr_d(obs), N, n,
+                                      ptr_d(est), ptr_d(res)))
+    return EstimationResult(est, res)
+
+
+def estimate_device(model: TrainedModel, obs, est=None, resid=None, stream=None,
+                    backend: Optional[BackendId] = None):
+    """Device-resident surveillance on torch CUDA tensors (N x n column-major,
+    i.e. tensors whose transpose is contiguous, or 1-D views with ld).
+
+    Asynchronous on ``stream`` (a torch.cuda.Stream, default: current)."""
+    import torch
+    backend = backend or model.backend
+    if obs.dim() != 2 or obs.stride(0) != 1:
+        raise ShapeError("estimate_device: observations must be column-major (N x n, stride(0)==1)")
+    N, n = obs.shape
+    ld = obs.stride(1) if n > 1 else N
+    dtype = {torch.float32: 1, torch.float64: 0}.get(obs.dtype)
+    if dtype is None:
+        raise ConfigError("estimate_device: observations must be float32 or float64")
+    ctx = _ctx(backend)
+    st = stream if stream is not None else torch.cuda.current_stream(obs.device)
+    ctx.set_stream(st.cuda_stream)
+    try:
+        check(_lib.lib().cs_mset_estimate_device(
+            ctx.handle, model.handle, C.c_void_p(obs.data_ptr()), dtype, N, n, ld,
+            C.c_void_p(est.data_ptr() if est is not None else 0),
+            C.c_void_p(resid.data_ptr() if resid is not None else 0)))
+    finally:
+        ctx.set_stream(None)

@@ -73,9 +73,11 @@ const char* cs_version(void);
 /* ----------------------------------------------------------- contexts */
 cs_status cs_ctx_create(int device, cs_ctx** out);
 cs_status cs_ctx_destroy(cs_ctx* ctx);
-/* Run on an external cudaStream_t (e.g. torch's current stream); NULL
- * restores the context's own stream. */
+/* Run on an external cudaStream_t (e.g. torch's current stream); NULL is
+ * the legacy default stream.  cs_ctx_reset_stream restores the context's
+ * own non-blocking stream. */
 cs_status cs_ctx_set_stream(cs_ctx* ctx, void* cuda_stream);
+cs_status cs_ctx_reset_stream(cs_ctx* ctx);
 cs_status cs_ctx_synchronize(cs_ctx* ctx);
 /* Device name / SM count / arithmetic description (BackendCapabilities,
  * backends.hpp:35-41). */

@@ -28,6 +28,7 @@ _SIGNATURES = {
     "cs_ctx_create": (i32, [i32, P(vp)]),
     "cs_ctx_destroy": (i32, [vp]),
     "cs_ctx_set_stream": (i32, [vp, vp]),
+    "cs_ctx_reset_stream": (i32, [vp]),
     "cs_ctx_synchronize": (i32, [vp]),
     "cs_ctx_describe": (i32, [vp, C.c_char_p, C.c_size_t]),
     "cs_sim_matrix": (i32, [vp, pd, pd, i64, i64, i64, i32, d, pd]),

@@ -46,8 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            *_sources(), "-o", LIB + ".tmp",
-           "-lcusolver", "-lcublas", "-lpthread",
-           "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+           "-lpthread", "-ldl"]
     subprocess.run(cmd, check=True, cwd=CSRC)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -15,11 +15,14 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <chrono>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "estimate_tc.cuh"
 #include "kernels_f64.cuh"
 #include "selection.cuh"
+#include "solver.cuh"
 
 using namespace csb;
 
@@ -87,7 +90,7 @@ struct cs_model {
   DevBuf<double> D, Dn, scale, pinv, spectrum;
   // FP32 tensor-core operands (precision == CS_PRECISION_FP32)
   bool tc = false;
-  int MT = 0, K1 = 0, N2 = 0, m_tiles = 0;
+  int MT = 0, NB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
   DevBuf<float> dn_tiles, p_tiles, dd, dn32, inv_scale, scale_f;
 };
 
@@ -212,17 +215,17 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
   std::memcpy(&asym, &hs[1], 8);
   if (asym > 1e-9 * std::max(mag, 1.0)) fail(CS_SHAPE_ERROR, "symmetric_eig: matrix is not symmetric to 1e-9");
   if (V != G) CSB_CUDA(cudaMemcpyAsync(V, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  solver_check(cusolverDnSetStream(ctx->solver, st), "SetStream");
+  const CusolverApi& api = cusolver_api();
+  if (!ctx->solver) solver_check(api.create(&ctx->solver), "cusolverDnCreate");
+  solver_check(api.set_stream(ctx->solver, st), "SetStream");
   int lwork = 0;
-  solver_check(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR,
-                                           CUBLAS_FILL_MODE_LOWER, static_cast<int>(m), V,
-                                           static_cast<int>(m), w, &lwork),
+  solver_check(api.syevd_buffer(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                static_cast<int>(m), V, static_cast<int>(m), w, &lwork),
                "Dsyevd_bufferSize");
   DevBuf<double> work(static_cast<size_t>(lwork) + 1);
   DevBuf<int> info(1);
-  solver_check(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
-                                static_cast<int>(m), V, static_cast<int>(m), w, work.get(), lwork,
-                                info.get()),
+  solver_check(api.syevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                         static_cast<int>(m), V, static_cast<int>(m), w, work.get(), lwork, info.get()),
                "Dsyevd");
   int hinfo = 0;
   CSB_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof hinfo, cudaMemcpyDeviceToHost, st));
@@ -235,13 +238,22 @@ void choose_tc_shape(cs_model* M) {
   M->K1 = static_cast<int>((M->n + 7) / 8 * 8);
   M->N2 = static_cast<int>((M->n + 15) / 16 * 16);
   M->MT = 0;
-  const int cand[4] = {128, 64, 32, 16};
-  for (int MT : cand) {
-    const int cols = M->N2 + 2 * M->K1 + 3 * MT;
+  // (memory tile MT, TMEM buffers NB) in order of preference.  A TS-form
+  // tcgen05.mma costs >= ~30 cycles whatever N (tools/mma_probe: N=16 and 32
+  // both 29.6 cycles, N=64 hits the 32-cycle M*N/256 floor), so GEMM1 tiles
+  // narrower than 64 waste the tensor pipe; double buffering (NB = 2)
+  // decouples the epilogue.  Then the deepest operand ring (<= 4) that fits.
+  const int pref[7][2] = {{128, 2}, {64, 2}, {128, 1}, {64, 1}, {32, 2}, {32, 1}, {16, 2}};
+  for (const auto& c : pref) {
+    const int MT = c[0], NB = c[1];
+    const int cols = tc_tmem_cols(M->N2, M->K1, MT, NB);
     const size_t stage = static_cast<size_t>(2) * MT * M->K1 * 4 + static_cast<size_t>(2) * M->N2 * MT * 4;
-    const size_t smem = 2 * stage + 256;
-    if (cols <= kTmemCols && smem <= 227 * 1024) {
+    const size_t budget = 227 * 1024 - tc_aux_bytes(M->K1);
+    const int stages = static_cast<int>(std::min<size_t>(kMaxStages, budget / stage));
+    if (cols <= kTmemCols && stages >= 2) {
       M->MT = MT;
+      M->NB = NB;
+      M->n_stages = stages;
       break;
     }
   }
@@ -278,8 +290,30 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
 }
 
 // ----------------------------------------------------------------- train
+// CSB_TRACE=1: synchronise and report the wall time of each train phase on
+// stderr (diagnostics; off by default).
+struct PhaseTrace {
+  bool on = false;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseTrace(cudaStream_t s) : st(s) {
+    const char* e = std::getenv("CSB_TRACE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[csb] %-24s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m, int kind,
                        double bandwidth, int precision) {
+  PhaseTrace trace(ctx->stream);
   check_kind(kind);
   if (precision != CS_PRECISION_FP64 && precision != CS_PRECISION_FP32)
     fail(CS_CONFIG_ERROR, "unknown precision");
@@ -291,7 +325,9 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->kind = kind;
   M->precision = precision;
   DevBuf<int64_t> picked;
+  trace.mark("enter");
   select_device(ctx, X, N, n, m, picked, M->source_indices);  // mset.cpp:142
+  trace.mark("select_memory_vectors");
   M->h = resolve_h(bandwidth, n);                            // mset.cpp:143-144
   M->D.resize(n * m);
   gather_memory_kernel<<<grid_for(n * m), 256, 0, st>>>(X, N, n, picked.get(), m, M->D.get());
@@ -303,9 +339,12 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   div_rows_kernel<<<grid_for(n * m), 256, 0, st>>>(M->D.get(), M->scale.get(), n, m, M->Dn.get());
   CSB_LAUNCH_CHECK();
   DevBuf<double> gram(m * m), V(m * m);                      // mset.cpp:151-152
+  trace.mark("scale + normalise");
   launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, kind, M->h, gram.get(), m);
+  trace.mark("gram (sim_exact)");
   M->spectrum.resize(m);                                     // mset.cpp:153-154
   eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get());
+  trace.mark("symmetric_eig (syevd)");
   M->spectrum_host.resize(m);
   CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
                            cudaMemcpyDeviceToHost, st));
@@ -321,8 +360,10 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   CSB_LAUNCH_CHECK();
   M->pinv.resize(m * m);
   launch_gemm_exact<false, true>(st, W.get(), m, W.get(), m, m, rank, m, M->pinv.get(), m);
+  trace.mark("pinv (W W^T)");
   if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
   CSB_CUDA(cudaStreamSynchronize(st));
+  trace.mark("fp32 operand packing");
   return M.release();
 }
 
@@ -391,7 +432,9 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   p.resid = resid;
   p.dn_stage_bytes = static_cast<uint32_t>(2 * M->MT * M->K1 * 4);
   p.p_stage_bytes = static_cast<uint32_t>(2 * M->N2 * M->MT * 4);
-  const size_t smem = 2 * (static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes) + 256;
+  p.n_stages = M->n_stages;
+  const size_t smem = M->n_stages * (static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes) +
+                      tc_aux_bytes(p.K1);
   const int tiles = static_cast<int>((N + kObsTile - 1) / kObsTile);
   const int grid = std::min(tiles, ctx->sm_count);
   auto go = [&](auto kernel) {
@@ -400,12 +443,15 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
     kernel<<<grid, kTcThreads, smem, st>>>(p);
     CSB_LAUNCH_CHECK();
   };
-  switch (M->MT) {
-    case 128: go(mset_estimate_tc_kernel<128, IO>); break;
-    case 64: go(mset_estimate_tc_kernel<64, IO>); break;
-    case 32: go(mset_estimate_tc_kernel<32, IO>); break;
-    case 16: go(mset_estimate_tc_kernel<16, IO>); break;
-    default: fail(CS_ERROR, "internal: bad tensor-core tile width");
+  switch (M->MT * 10 + M->NB) {
+    case 1282: go(mset_estimate_tc_kernel<128, 2, IO>); break;
+    case 642: go(mset_estimate_tc_kernel<64, 2, IO>); break;
+    case 1281: go(mset_estimate_tc_kernel<128, 1, IO>); break;
+    case 641: go(mset_estimate_tc_kernel<64, 1, IO>); break;
+    case 322: go(mset_estimate_tc_kernel<32, 2, IO>); break;
+    case 321: go(mset_estimate_tc_kernel<32, 1, IO>); break;
+    case 162: go(mset_estimate_tc_kernel<16, 2, IO>); break;
+    default: fail(CS_ERROR, "internal: bad tensor-core tile shape");
   }
 }
 
@@ -459,8 +505,7 @@ cs_status cs_ctx_create(int device, cs_ctx** out) {
     CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking));
     CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
     c->stream = c->own;
-    solver_check(cusolverDnCreate(&c->solver), "cusolverDnCreate");
-    *out = c.release();
+    *out = c.release();  // cuSOLVER handle created on the first eigendecomposition
   });
 }
 
@@ -469,7 +514,7 @@ cs_status cs_ctx_destroy(cs_ctx* ctx) {
     if (!ctx) return;
     set_device(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    if (ctx->solver) cusolver_api().destroy(ctx->solver);
     for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1]})
       if (s) cudaStreamDestroy(s);
     delete ctx;
@@ -479,7 +524,14 @@ cs_status cs_ctx_destroy(cs_ctx* ctx) {
 cs_status cs_ctx_set_stream(cs_ctx* ctx, void* stream) {
   return guarded([&] {
     if (!ctx) fail(CS_CONFIG_ERROR, "null context");
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+cs_status cs_ctx_reset_stream(cs_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(CS_CONFIG_ERROR, "null context");
+    ctx->stream = ctx->own;
   });
 }
 

@@ -10,17 +10,20 @@
 // mset.cpp:189-191).
 //
 // One CTA (persistent, grid = #SMs) owns a 128-observation tile at a time and
-// streams the memory matrix in MT-wide tiles.  Warp roles:
-//   warp 0      producer: 1D bulk copies (TMA engine) of pre-tiled D_norm^T and
-//               P^T operand tiles into a 2-deep shared-memory ring each
-//   warp 1      MMA issuer (one thread): tcgen05.mma kind::tf32
-//   warps 2..5  epilogue: x prologue, TMEM->reg kernel map, reg->TMEM S,
-//               final estimate / residual stores
+// streams the memory matrix in MT-wide tiles ("steps").  Warp roles:
+//   warp 0       producer: 1D bulk copies (TMA engine) of pre-tiled D_norm^T
+//                and P^T operand tiles into n_stages-deep shared-memory rings
+//   warp 1       MMA issuer (one thread): tcgen05.mma kind::tf32.  GEMM1 runs
+//                two steps ahead of GEMM2.
+//   warps 2..17  epilogue: two sets of 8 warps; set e owns the steps with
+//                j % 2 == e (and TMEM buffer e), each warp a 32-lane quarter
+//                and half of the MT columns.  All 16 warps share the x
+//                prologue and the final estimate / residual readout.
 // TMEM (512 columns x 128 lanes, lane = observation):
-//   [0, N2)             O   = S P^T accumulator          (GEMM2 D)
-//   [N2, N2+2K1)        X   = x_norm hi | lo              (GEMM1 A, "TS" form)
-//   [.., +MT)           ACC = X D_norm accumulator         (GEMM1 D)
-//   [.., +2MT)          S   = similarity hi | lo           (GEMM2 A, "TS" form)
+//   O   [N2]            S P^T accumulator                 (GEMM2 D)
+//   X   [2 K1]          x_norm hi | lo                    (GEMM1 A, "TS" form)
+//   ACC [2 x MT]        X D_norm accumulators             (GEMM1 D)
+//   S   [2 x 2 MT]      similarity hi | lo                (GEMM2 A, "TS" form)
 // FP32-accurate products on TF32 hardware: every operand v is split into
 // hi = rna_tf32(v), lo = v - hi and each GEMM issues hi*hi + hi*lo + lo*hi
 // (3xTF32).  Single-pass TF32 misses the 1e-3 tolerance.
@@ -30,18 +33,23 @@
 #pragma once
 
 #include "common.cuh"
+#include "pack_tc.cuh"
 #include "sm100_ptx.cuh"
 
 namespace csb {
 
-constexpr int kTcThreads = 192;
+constexpr int kEpiWarps = 16;
+constexpr int kEpiThreads = 32 * kEpiWarps;         // 512
+constexpr int kTcThreads = 64 + kEpiThreads;        // 576
 constexpr int kObsTile = 128;
 constexpr int kTmemCols = 512;
+constexpr int kMaxStages = 4;
 
 struct TcParams {
   const void* obs;  // N x n, leading dim ld, IO type
   int64_t N, ld;
   int n, K1, N2, m, m_tiles;
+  int n_stages;
   const float* dn_tiles;  // m_tiles x [hi | lo] (MT x K1 canonical K-major)
   const float* p_tiles;   // m_tiles x [hi | lo] (N2 x MT canonical K-major)
   const float* dd;        // m_tiles*MT squared norms of D_norm columns (0 padded)
@@ -58,48 +66,85 @@ struct TcParams {
   uint32_t dn_stage_bytes, p_stage_bytes;
 };
 
-template <typename IO>
-__device__ __forceinline__ float load_norm(const IO* obs, int64_t idx, int s,
-                                           const TcParams& p) {
-  if constexpr (sizeof(IO) == 8) {
-    return static_cast<float>(static_cast<double>(obs[idx]) / p.scale_d[s]);
-  } else {
-    return static_cast<float>(obs[idx]) * p.inv_scale[s];
-  }
+// TMEM columns used for a given shape and buffer count NB (1 or 2).
+__host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB) {
+  return N2 + 2 * K1 + NB * MT + NB * 2 * MT;
 }
 
-template <int MT, typename IO>
+// Shared-memory footprint of everything but the operand rings: barriers,
+// staged scales and the per-row ||x||^2 partials.
+__host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
+  return 512 + static_cast<size_t>(K1) * (4 + 4 + 8 + 8) + 4 * kObsTile * 4;
+}
+
+// ring position: (index, phase) advanced in issue order
+struct Ring {
+  uint32_t idx = 0, phase = 0, n = 1;
+  __device__ explicit Ring(uint32_t n_) : n(n_) {}
+  __device__ void next() {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+// NB = 2: double-buffered ACC / S, two epilogue sets alternate steps, GEMM1
+//         two steps ahead.  NB = 1: single buffers, all 16 epilogue warps
+//         work on every step (4 column groups), GEMM1 one step ahead.
+template <int MT, int NB, typename IO>
 __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const TcParams p) {
+  static_assert(NB == 1 || NB == 2, "one or two TMEM buffers");
+  constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
+  constexpr int kLookahead = NB;                 // GEMM1 steps ahead of GEMM2
+  constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
+  constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
+  static_assert(COLS % 8 == 0, "epilogue column slice must be a multiple of 8");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int NS = p.n_stages;
   uint8_t* dn_ring = smem;
-  uint8_t* p_ring = smem + 2 * p.dn_stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p_ring + 2 * p.p_stage_bytes);
-  uint64_t* dn_full = bars + 0;
-  uint64_t* dn_empty = bars + 2;
-  uint64_t* p_full = bars + 4;
-  uint64_t* p_empty = bars + 6;
-  uint64_t* x_ready = bars + 8;
-  uint64_t* x_free = bars + 9;
-  uint64_t* acc_full = bars + 10;
-  uint64_t* acc_free = bars + 11;
-  uint64_t* s_ready = bars + 12;
-  uint64_t* s_free = bars + 13;
-  uint64_t* o_full = bars + 14;
-  uint64_t* o_free = bars + 15;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
+  uint8_t* p_ring = smem + NS * p.dn_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p_ring + NS * p.p_stage_bytes);
+  uint64_t* dn_full = bars + 0;    // [4]
+  uint64_t* dn_empty = bars + 4;   // [4]
+  uint64_t* p_full = bars + 8;     // [4]
+  uint64_t* p_empty = bars + 12;   // [4]
+  uint64_t* acc_full = bars + 16;  // [2]
+  uint64_t* acc_free = bars + 18;  // [2]
+  uint64_t* s_ready = bars + 20;   // [2]
+  uint64_t* s_free = bars + 22;    // [2]
+  uint64_t* x_ready = bars + 24;
+  uint64_t* x_free = bars + 25;
+  uint64_t* o_full = bars + 26;
+  uint64_t* o_free = bars + 27;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
+  double* s_inv_d = reinterpret_cast<double*>(bars + 64);
+  double* s_scale_d = s_inv_d + p.K1;
+  float* s_inv_f = reinterpret_cast<float*>(s_scale_d + p.K1);
+  float* s_scale_f = s_inv_f + p.K1;
+  float* s_xx = s_scale_f + p.K1;  // [4][kObsTile]
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 8; ++i) ptx::mbar_init(&bars[i], 1);
-    ptx::mbar_init(x_ready, 4);
+    for (int i = 0; i < 16; ++i) ptx::mbar_init(&bars[i], 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&acc_full[b], 1);
+      ptx::mbar_init(&acc_free[b], kSetWarps);
+      ptx::mbar_init(&s_ready[b], kSetWarps);
+      ptx::mbar_init(&s_free[b], 1);
+    }
+    ptx::mbar_init(x_ready, kEpiWarps);
     ptx::mbar_init(x_free, 1);
-    ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(acc_free, 4);
-    ptx::mbar_init(s_ready, 4);
-    ptx::mbar_init(s_free, 1);
     ptx::mbar_init(o_full, 1);
-    ptx::mbar_init(o_free, 4);
+    ptx::mbar_init(o_free, kEpiWarps);
     ptx::fence_mbar_init();
+  }
+  for (int s = threadIdx.x; s < p.K1; s += blockDim.x) {
+    const bool ok = s < p.n;
+    s_inv_d[s] = ok ? 1.0 / p.scale_d[s] : 0.0;
+    s_scale_d[s] = ok ? p.scale_d[s] : 0.0;
+    s_inv_f[s] = ok ? p.inv_scale[s] : 0.f;
+    s_scale_f[s] = ok ? p.scale_f[s] : 0.f;
   }
   if (warp == 0) ptx::tmem_alloc(tmem_holder, kTmemCols);
   ptx::tc_fence_before();
@@ -110,305 +155,352 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
   const int K1 = p.K1, N2 = p.N2;
   const uint32_t colO = 0;
   const uint32_t colXh = N2, colXl = N2 + K1;
-  const uint32_t colS = N2 + 2 * K1;
-  const uint32_t colSh = colS + MT, colSl = colS + 2 * MT;
+  const uint32_t colAcc = N2 + 2 * K1;   // + b*MT
+  const uint32_t colS = colAcc + NB * MT;  // + b*2MT (hi), + MT (lo)
   const int n_tiles = static_cast<int>((p.N + kObsTile - 1) / kObsTile);
+  const int T = p.m_tiles;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      uint32_t g = 0;
+    // (whole warp, converged; one elected lane issues)
+    {
+      Ring r(NS);
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        for (int j = 0; j < p.m_tiles; ++j, ++g) {
-          const uint32_t st = g & 1, u = g >> 1;
-          ptx::mbar_wait(&dn_empty[st], (u & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&dn_full[st], p.dn_stage_bytes);
-          ptx::bulk_g2s(dn_ring + st * p.dn_stage_bytes,
-                        p.dn_tiles + static_cast<size_t>(j) * (p.dn_stage_bytes / 4),
-                        p.dn_stage_bytes, &dn_full[st]);
-          ptx::mbar_wait(&p_empty[st], (u & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&p_full[st], p.p_stage_bytes);
-          ptx::bulk_g2s(p_ring + st * p.p_stage_bytes,
-                        p.p_tiles + static_cast<size_t>(j) * (p.p_stage_bytes / 4),
-                        p.p_stage_bytes, &p_full[st]);
+        for (int j = 0; j < T; ++j, r.next()) {
+          ptx::mbar_wait(&dn_empty[r.idx], r.phase ^ 1);
+          ptx::mbar_arrive_expect_tx_elect(&dn_full[r.idx], p.dn_stage_bytes);
+          ptx::bulk_g2s_elect(dn_ring + r.idx * p.dn_stage_bytes,
+                              p.dn_tiles + static_cast<size_t>(j) * (p.dn_stage_bytes / 4),
+                              p.dn_stage_bytes, &dn_full[r.idx]);
+          ptx::mbar_wait(&p_empty[r.idx], r.phase ^ 1);
+          ptx::mbar_arrive_expect_tx_elect(&p_full[r.idx], p.p_stage_bytes);
+          ptx::bulk_g2s_elect(p_ring + r.idx * p.p_stage_bytes,
+                              p.p_tiles + static_cast<size_t>(j) * (p.p_stage_bytes / 4),
+                              p.p_stage_bytes, &p_full[r.idx]);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // (whole warp, converged, warp-uniform operands; one elected lane issues)
+    {
       const uint32_t idesc1 = ptx::idesc_tf32(128, MT);
       const uint32_t idesc2 = ptx::idesc_tf32(128, N2);
       const uint32_t SBO = 128;
       const uint32_t LBO1 = (MT / 8) * 128;  // D_norm^T tile: MT rows x K1
       const uint32_t LBO2 = (N2 / 8) * 128;  // P^T tile: N2 rows x MT
-      uint32_t g1 = 0, g2 = 0, tcount = 0;
-      auto issue_g2 = [&](int jj) {
-        const uint32_t st = g2 & 1, u = g2 >> 1;
-        ptx::mbar_wait(s_ready, g2 & 1);
-        ptx::mbar_wait(&p_full[st], u & 1);
-        if (jj == 0) ptx::mbar_wait(o_free, (tcount & 1) ^ 1);
+      const uint64_t dn_desc0 = ptx::smem_desc(ptx::smem_u32(dn_ring), LBO1, SBO);
+      const uint64_t p_desc0 = ptx::smem_desc(ptx::smem_u32(p_ring), LBO2, SBO);
+      const uint64_t dn_lo_off = (static_cast<uint64_t>(MT) * K1 * 4) >> 4;
+      const uint64_t p_lo_off = (static_cast<uint64_t>(N2) * MT * 4) >> 4;
+      const uint64_t dn_stage_off = p.dn_stage_bytes >> 4, p_stage_off = p.p_stage_bytes >> 4;
+      const uint64_t k_step1 = (2 * LBO1) >> 4, k_step2 = (2 * LBO2) >> 4;
+      const uint32_t dO = tmem + colO;
+      Ring rd(NS), rp(NS);
+      uint32_t acc_use[2] = {0, 0}, s_use[2] = {0, 0};
+      uint32_t tcount1 = 0, tcount2 = 0;
+
+      auto issue_g1 = [&](int j) {
+        const int b = NB == 2 ? (j & 1) : 0;
+        if (j == 0) ptx::mbar_wait(x_ready, tcount1 & 1);
+        ptx::mbar_wait(&dn_full[rd.idx], rd.phase);
+        ptx::mbar_wait(&acc_free[b], (acc_use[b] & 1) ^ 1);
         ptx::tc_fence_after();
-        const uint32_t hi = ptx::smem_u32(p_ring + st * p.p_stage_bytes);
-        const uint32_t lo = hi + N2 * MT * 4;
+        const uint32_t dS = tmem + colAcc + b * MT;
+        uint64_t bh = dn_desc0 + rd.idx * dn_stage_off;
+        uint64_t bl = bh + dn_lo_off;
+        uint32_t ah = tmem + colXh, al = tmem + colXl;
+        for (int kk = 0; kk < K1 / 8; ++kk) {
+          ptx::mma_tf32_ts_elect(dS, al, bh, idesc1, kk > 0 ? 1u : 0u);
+          ptx::mma_tf32_ts_elect(dS, ah, bl, idesc1, 1u);
+          ptx::mma_tf32_ts_elect(dS, ah, bh, idesc1, 1u);
+          bh += k_step1;
+          bl += k_step1;
+          ah += 8;
+          al += 8;
+        }
+        ptx::tc_commit_elect(&acc_full[b]);
+        ptx::tc_commit_elect(&dn_empty[rd.idx]);
+        if (j == T - 1) {
+          ptx::tc_commit_elect(x_free);
+          ++tcount1;
+        }
+        ++acc_use[b];
+        rd.next();
+      };
+      auto issue_g2 = [&](int j) {
+        const int b = NB == 2 ? (j & 1) : 0;
+        ptx::mbar_wait(&s_ready[b], s_use[b] & 1);
+        ptx::mbar_wait(&p_full[rp.idx], rp.phase);
+        if (j == 0) ptx::mbar_wait(o_free, (tcount2 & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint64_t bh0 = p_desc0 + rp.idx * p_stage_off;
+        const uint64_t bl0 = bh0 + p_lo_off;
+        uint32_t ah = tmem + colS + b * 2 * MT;
+        uint32_t al = ah + MT;
 #pragma unroll
         for (int kk = 0; kk < MT / 8; ++kk) {
-          const uint64_t bh = ptx::smem_desc(hi + kk * 2 * LBO2, LBO2, SBO);
-          const uint64_t bl = ptx::smem_desc(lo + kk * 2 * LBO2, LBO2, SBO);
-          const uint32_t ah = tmem + colSh + kk * 8, al = tmem + colSl + kk * 8;
-          const uint32_t first = (jj == 0 && kk == 0);
-          ptx::mma_tf32_ts(tmem + colO, al, bh, idesc2, first ? 0u : 1u);
-          ptx::mma_tf32_ts(tmem + colO, ah, bl, idesc2, 1u);
-          ptx::mma_tf32_ts(tmem + colO, ah, bh, idesc2, 1u);
+          const uint64_t bh = bh0 + kk * k_step2, bl = bl0 + kk * k_step2;
+          ptx::mma_tf32_ts_elect(dO, al, bh, idesc2, (j == 0 && kk == 0) ? 0u : 1u);
+          ptx::mma_tf32_ts_elect(dO, ah, bl, idesc2, 1u);
+          ptx::mma_tf32_ts_elect(dO, ah, bh, idesc2, 1u);
+          ah += 8;
+          al += 8;
         }
-        ptx::tc_commit(s_free);
-        ptx::tc_commit(&p_empty[st]);
-        ++g2;
+        ptx::tc_commit_elect(&s_free[b]);
+        ptx::tc_commit_elect(&p_empty[rp.idx]);
+        if (j == T - 1) {
+          ptx::tc_commit_elect(o_full);
+          ++tcount2;
+        }
+        ++s_use[b];
+        rp.next();
       };
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-        ptx::mbar_wait(x_ready, tcount & 1);
-        for (int j = 0; j < p.m_tiles; ++j) {
-          const uint32_t st = g1 & 1, u = g1 >> 1;
-          ptx::mbar_wait(&dn_full[st], u & 1);
-          ptx::mbar_wait(acc_free, (g1 & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t hi = ptx::smem_u32(dn_ring + st * p.dn_stage_bytes);
-          const uint32_t lo = hi + MT * K1 * 4;
-          for (int kk = 0; kk < K1 / 8; ++kk) {
-            const uint64_t bh = ptx::smem_desc(hi + kk * 2 * LBO1, LBO1, SBO);
-            const uint64_t bl = ptx::smem_desc(lo + kk * 2 * LBO1, LBO1, SBO);
-            const uint32_t ah = tmem + colXh + kk * 8, al = tmem + colXl + kk * 8;
-            ptx::mma_tf32_ts(tmem + colS, al, bh, idesc1, kk > 0 ? 1u : 0u);
-            ptx::mma_tf32_ts(tmem + colS, ah, bl, idesc1, 1u);
-            ptx::mma_tf32_ts(tmem + colS, ah, bh, idesc1, 1u);
-          }
-          ptx::tc_commit(acc_full);
-          ptx::tc_commit(&dn_empty[st]);
-          if (j == p.m_tiles - 1) ptx::tc_commit(x_free);
-          ++g1;
-          if (j >= 1) issue_g2(j - 1);
+
+      const int prime = T < kLookahead ? T : kLookahead;
+      if (static_cast<int>(blockIdx.x) < n_tiles)
+        for (int k = 0; k < prime; ++k) issue_g1(k);
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int j = 0; j < T; ++j) {
+          if (j + kLookahead < T) issue_g1(j + kLookahead);
+          issue_g2(j);
         }
-        issue_g2(p.m_tiles - 1);
-        ptx::tc_commit(o_full);
+        if (tile + static_cast<int>(gridDim.x) < n_tiles)
+          for (int k = 0; k < prime; ++k) issue_g1(k);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 2;               // 0..15
+    const int q = warp & 3;                // TMEM lane quarter this warp may access
+    const int set = NB == 2 ? (ew >> 3) : 0;                // step parity owned
+    const int half = NB == 2 ? ((ew >> 2) & 1) : (ew >> 2);  // column slice in step
+    const int g4 = ew >> 2;                // 0..3 for prologue / readout split
     const int row = 32 * q + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     const IO* obs = static_cast<const IO*>(p.obs);
     IO* est = static_cast<IO*>(p.est);
     IO* resid = static_cast<IO*>(p.resid);
+    const bool gaussian = p.kind == CS_KERNEL_GAUSSIAN;
+    const int c0 = half * COLS;
+
+    // normalised observation value (branch-free: out-of-range reads element 0)
+    auto xnorm = [&](int64_t t, int s, bool valid) -> float {
+      const bool ok = valid && s < p.n;
+      const IO raw = obs[ok ? t + static_cast<int64_t>(s) * p.ld : 0];
+      float v;
+      if constexpr (sizeof(IO) == 8) {
+        v = static_cast<float>(static_cast<double>(raw) * s_inv_d[s]);
+      } else {
+        v = static_cast<float>(raw) * s_inv_f[s];
+      }
+      return ok ? v : 0.f;
+    };
 
     uint32_t prologue_count = 0;
-    auto prologue = [&](int tile, float& xx) {
+    // x prologue: warp group g4 normalises, splits and stores K-chunks
+    // k8 = g4 mod 4 and contributes a partial ||x||^2 for its chunks.
+    auto prologue = [&](int tile) {
       ptx::mbar_wait(x_free, (prologue_count & 1) ^ 1);
       ++prologue_count;
       ptx::tc_fence_after();
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
       float acc = 0.f;
-      for (int k8 = 0; k8 < K1 / 8; ++k8) {
+      for (int k8 = g4; k8 < K1 / 8; k8 += 4) {
+        float xv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = xnorm(t, k8 * 8 + e, valid);
         uint32_t hi[8], lo[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int s = k8 * 8 + e;
-          float xv = 0.f;
-          if (valid && s < p.n) xv = load_norm<IO>(obs, t + static_cast<int64_t>(s) * p.ld, s, p);
-          acc = fmaf(xv, xv, acc);
-          const uint32_t h = ptx::to_tf32(xv);
+          acc = fmaf(xv[e], xv[e], acc);
+          const uint32_t h = ptx::to_tf32(xv[e]);
           hi[e] = h;
-          lo[e] = __float_as_uint(xv - __uint_as_float(h));
+          lo[e] = __float_as_uint(xv[e] - __uint_as_float(h));
         }
         ptx::tmem_st8(tmem + lane_off + colXh + k8 * 8, hi);
         ptx::tmem_st8(tmem + lane_off + colXl + k8 * 8, lo);
       }
-      xx = acc;
+      s_xx[g4 * kObsTile + row] = acc;
       ptx::tc_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(x_ready);
     };
+    auto gather_xx = [&]() -> float {
+      ptx::named_bar_sync(1, kEpiThreads);
+      float xx = 0.f;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) xx += s_xx[g * kObsTile + row];
+      ptx::named_bar_sync(1, kEpiThreads);  // partials may be overwritten afterwards
+      return xx;
+    };
 
-    uint32_t g = 0, tcount = 0;
-    float xx_cur = 0.f, xx_next = 0.f;
-    if (static_cast<int>(blockIdx.x) < n_tiles) prologue(blockIdx.x, xx_cur);
+    uint32_t use = 0, tcount = 0;  // uses of this set's TMEM buffers
+    float xx_cur = 0.f;
+    if (static_cast<int>(blockIdx.x) < n_tiles) {
+      prologue(blockIdx.x);
+      xx_cur = gather_xx();
+    }
+    const uint32_t a_base = colAcc + set * MT + c0;
+    const uint32_t s_base = colS + set * 2 * MT + c0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
-      for (int j = 0; j < p.m_tiles; ++j, ++g) {
-        float v[MT];
-        ptx::mbar_wait(acc_full, g & 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < MT / 16; ++c) ptx::tmem_ld16(tmem + lane_off + colS + c * 16, &v[c * 16]);
-        ptx::tc_wait_ld();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(acc_free);
-
-        const float* dd = p.dd + static_cast<size_t>(j) * MT;
-#pragma unroll
-        for (int c = 0; c < MT; ++c) {
-          const int mem = j * MT + c;
-          const float ddc = __ldg(dd + c);
-          const float base = xx_cur + ddc;
-          float d2 = fmaf(-2.f, v[c], base);
-          if (d2 < p.tau * base && valid && mem < p.m) {
-            // direct difference (rare): cancellation-free d2
-            float a = 0.f;
-            for (int s = 0; s < p.n; ++s) {
-              const float xv = load_norm<IO>(obs, t + static_cast<int64_t>(s) * p.ld, s, p);
-              const float dv = __ldg(p.dn32 + static_cast<size_t>(mem) * p.n + s);
-              const float d = xv - dv;
-              a = fmaf(d, d, a);
-            }
-            d2 = a;
-          }
-          d2 = fmaxf(d2, 0.f);
-          float sv;
-          if (p.kind == CS_KERNEL_GAUSSIAN) {
-            sv = exp2f(-d2 * p.g_coef);
+      for (int j = set; j < T; j += NB, ++use) {
+        const int valid_cols = min(COLS, p.m - (j * MT + c0));
+        const float* dd = p.dd + static_cast<size_t>(j) * MT + c0;
+        // ACC chunk c -> similarity values in v[0..CH)
+        auto compute_chunk = [&](int c, float* v) {
+          if constexpr (CH == 16) {
+            ptx::tmem_ld16_wait(tmem + lane_off + a_base + c * CH, v);
           } else {
-            const float r = d2 > 0.f ? d2 * rsqrtf(d2) : 0.f;
-            sv = __fdividef(1.f, fmaf(r, p.inv_h, 1.f));
+            ptx::tmem_ld8_wait(tmem + lane_off + a_base + c * CH, v);
           }
-          v[c] = mem < p.m ? sv : 0.f;
-        }
-        ptx::mbar_wait(s_free, (g & 1) ^ 1);
+          float ddv[CH];
+#pragma unroll
+          for (int e = 0; e < CH / 4; ++e) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(dd + c * CH) + e);
+            ddv[4 * e] = w.x;
+            ddv[4 * e + 1] = w.y;
+            ddv[4 * e + 2] = w.z;
+            ddv[4 * e + 3] = w.w;
+          }
+          // d2 in GEMM form; track the smallest margin to the cancellation guard
+          float margin = 1.f;
+#pragma unroll
+          for (int e = 0; e < CH; ++e) {
+            const float base = xx_cur + ddv[e];
+            const float d2 = fmaf(-2.f, v[e], base);
+            margin = fminf(margin, fmaf(-p.tau, base, d2));
+            v[e] = d2;
+          }
+          if (margin < 0.f && valid) {  // rare: direct difference, not unrolled
+#pragma unroll 1
+            for (int e = 0; e < CH; ++e) {
+              float base = 0.f, cur = 0.f;
+#pragma unroll
+              for (int ee = 0; ee < CH; ++ee)
+                if (ee == e) { base = xx_cur + ddv[ee]; cur = v[ee]; }
+              const int col = c * CH + e;
+              if (col >= valid_cols || !(cur < p.tau * base)) continue;
+              const int mem = j * MT + c0 + col;
+              float a = 0.f;
+              for (int s = 0; s < p.n; ++s) {
+                const float d = xnorm(t, s, true) - __ldg(p.dn32 + static_cast<size_t>(mem) * p.n + s);
+                a = fmaf(d, d, a);
+              }
+#pragma unroll
+              for (int ee = 0; ee < CH; ++ee)
+                if (ee == e) v[ee] = a;
+            }
+          }
+          if (gaussian) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e) v[e] = ptx::ex2_approx(-fmaxf(v[e], 0.f) * p.g_coef);
+          } else {
+#pragma unroll
+            for (int e = 0; e < CH; ++e) {
+              const float d2 = fmaxf(v[e], 1e-30f);
+              const float r = d2 * ptx::rsqrt_approx(d2);
+              v[e] = ptx::rcp_approx(fmaf(r, p.inv_h, 1.f));
+            }
+          }
+          if (valid_cols < (c + 1) * CH) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e)
+              if (c * CH + e >= valid_cols) v[e] = 0.f;
+          }
+        };
+        // v[0..CH) -> TMEM S hi | lo
+        auto store_chunk = [&](int c, const float* v) {
+#pragma unroll
+          for (int h8 = 0; h8 < CH / 8; ++h8) {
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float sv = v[h8 * 8 + e];
+              const uint32_t h = ptx::to_tf32(sv);
+              hi[e] = h;
+              lo[e] = __float_as_uint(sv - __uint_as_float(h));
+            }
+            ptx::tmem_st8(tmem + lane_off + s_base + c * CH + h8 * 8, hi);
+            ptx::tmem_st8(tmem + lane_off + s_base + MT + c * CH + h8 * 8, lo);
+          }
+        };
+        ptx::mbar_wait(&acc_full[set], use & 1);
         ptx::tc_fence_after();
+        if constexpr (NB == 1) {
+          // single buffers: release ACC as early as possible (GEMM1 of the
+          // next step may start), then wait for GEMM2 of the previous step
+          // before overwriting S
+          float vall[COLS];
 #pragma unroll
-        for (int c = 0; c < MT / 16; ++c) {
-          uint32_t hi[16], lo[16];
+          for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
+          ptx::mbar_wait(&s_free[set], (use & 1) ^ 1);
+          ptx::tc_fence_after();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float sv = v[c * 16 + e];
-            const uint32_t h = ptx::to_tf32(sv);
-            hi[e] = h;
-            lo[e] = __float_as_uint(sv - __uint_as_float(h));
+          for (int c = 0; c < COLS / CH; ++c) store_chunk(c, vall + c * CH);
+        } else {
+          // double buffers: S(j-2) was consumed long ago; stream chunk by chunk
+          ptx::mbar_wait(&s_free[set], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < COLS / CH; ++c) {
+            float v[CH];
+            compute_chunk(c, v);
+            store_chunk(c, v);
           }
-          ptx::tmem_st16(tmem + lane_off + colSh + c * 16, hi);
-          ptx::tmem_st16(tmem + lane_off + colSl + c * 16, lo);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_free[set]);  // all ACC chunks loaded
         }
         ptx::tc_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(s_ready);
+        if (lane == 0) ptx::mbar_arrive(&s_ready[set]);
       }
       // next tile's x prologue overlaps this tile's last GEMM2
       const int next = tile + gridDim.x;
-      if (next < n_tiles) prologue(next, xx_next);
+      if (next < n_tiles) prologue(next);
 
       // readout: estimate = scale .* O, residual = x - estimate
       ptx::mbar_wait(o_full, tcount & 1);
       ptx::tc_fence_after();
-      for (int c = 0; c < N2 / 16; ++c) {
-        float o[16];
-        ptx::tmem_ld16(tmem + lane_off + colO + c * 16, o);
-        ptx::tc_wait_ld();
-        if (valid) {
+      for (int c = g4; c < N2 / 8; c += 4) {
+        float o[8];
+        ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int s = c * 16 + e;
-            if (s < p.n) {
-              const int64_t idx = t + static_cast<int64_t>(s) * p.ld;
-              if constexpr (sizeof(IO) == 8) {
-                const double ev = static_cast<double>(o[e]) * p.scale_d[s];
-                if (est) est[idx] = ev;
-                if (resid) resid[idx] = static_cast<double>(obs[idx]) - ev;
-              } else {
-                const float ev = o[e] * p.scale_f[s];
-                if (est) est[idx] = ev;
-                if (resid) resid[idx] = static_cast<float>(obs[idx]) - ev;
-              }
-            }
+        for (int e = 0; e < 8; ++e) {
+          const int s = c * 8 + e;
+          const bool ok = valid && s < p.n;
+          const int64_t idx = ok ? t + static_cast<int64_t>(s) * p.ld : 0;
+          const IO x = obs[idx];
+          if constexpr (sizeof(IO) == 8) {
+            const double ev = static_cast<double>(o[e]) * s_scale_d[s];
+            if (ok && est) est[idx] = ev;
+            if (ok && resid) resid[idx] = x - ev;
+          } else {
+            const float ev = o[e] * s_scale_f[s];
+            if (ok && est) est[idx] = ev;
+            if (ok && resid) resid[idx] = x - ev;
           }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(o_free);
-      xx_cur = xx_next;
+      if (next < n_tiles) xx_cur = gather_xx();
     }
   }
   __syncthreads();
   if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTmemCols);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Operand pre-tiling (once per model, at train time).  Canonical K-major,
-// no-swizzle layout: element (r, k) of an R x K block sits at byte
-//   (r%8)*16 + (r/8)*128 + (k%4)*4 + (k/4)*LBO,  LBO = (R/8)*128.
-__device__ __forceinline__ size_t canon_off(int r, int k, int R) {
-  return static_cast<size_t>((r & 7) * 4 + (r >> 3) * 32 + (k & 3) + (k >> 2) * (R / 8) * 32);
-}
-
-// D_norm^T tiles: block j holds memory vectors j*MT.. as rows, signals as K.
-__global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m, int MT, int K1,
-                                     int m_tiles, float* __restrict__ out) {
-  const int64_t per = static_cast<int64_t>(MT) * K1;
-  const int64_t total = per * m_tiles;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e / per);
-    const int rem = static_cast<int>(e % per);
-    const int r = rem % MT, k = rem / MT;
-    const int mem = j * MT + r;
-    const double v = (k < n && mem < m) ? Dn[k + static_cast<int64_t>(mem) * n] : 0.0;
-    const float f = static_cast<float>(v);
-    const float hi = __uint_as_float(ptx::to_tf32(f));
-    const float lo = static_cast<float>(v - static_cast<double>(hi));
-    float* blk = out + static_cast<size_t>(j) * 2 * per;
-    blk[canon_off(r, k, MT)] = hi;
-    blk[per + canon_off(r, k, MT)] = lo;
-  }
-}
-
-// P^T tiles: block j holds signals as rows (N2), memory vectors j*MT.. as K.
-__global__ void pack_p_tiles_kernel(const double* __restrict__ P, int n, int m, int MT, int N2,
-                                    int m_tiles, float* __restrict__ out) {
-  const int64_t per = static_cast<int64_t>(N2) * MT;
-  const int64_t total = per * m_tiles;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e / per);
-    const int rem = static_cast<int>(e % per);
-    const int r = rem % N2, k = rem / N2;
-    const int mem = j * MT + k;
-    const double v = (r < n && mem < m) ? P[r + static_cast<int64_t>(mem) * n] : 0.0;
-    const float f = static_cast<float>(v);
-    const float hi = __uint_as_float(ptx::to_tf32(f));
-    const float lo = static_cast<float>(v - static_cast<double>(hi));
-    float* blk = out + static_cast<size_t>(j) * 2 * per;
-    blk[canon_off(r, k, N2)] = hi;
-    blk[per + canon_off(r, k, N2)] = lo;
-  }
-}
-
-// ||D_norm(:, c)||^2 (FP64 -> FP32, zero padded), D_norm in FP32, 1/scale.
-__global__ void pack_aux_kernel(const double* __restrict__ Dn, const double* __restrict__ scale,
-                                int n, int m, int m_pad, float* __restrict__ dd,
-                                float* __restrict__ dn32, float* __restrict__ inv_scale,
-                                float* __restrict__ scale_f) {
-  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t c = tid; c < m_pad; c += stride) {
-    double a = 0.0;
-    if (c < m)
-      for (int s = 0; s < n; ++s) {
-        const double v = Dn[s + c * n];
-        a = fma(v, v, a);
-      }
-    dd[c] = static_cast<float>(a);
-  }
-  for (int64_t e = tid; e < static_cast<int64_t>(n) * m; e += stride) dn32[e] = static_cast<float>(Dn[e]);
-  for (int64_t s = tid; s < n; s += stride) {
-    inv_scale[s] = static_cast<float>(1.0 / scale[s]);
-    scale_f[s] = static_cast<float>(scale[s]);
   }
 }
 

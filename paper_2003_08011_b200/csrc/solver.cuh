@@ -1,0 +1,73 @@
+// solver.cuh -- lazily bound cuSOLVER entry points for the FP64 symmetric
+// eigendecomposition (symmetric_eig, mset.cpp:57-70).
+//
+// cuSOLVER and its dependencies (cuBLAS / cuBLASLt / cuSPARSE / nvJitLink,
+// ~1.5 GB) are not linked at load time: on a cold box, mapping them costs
+// minutes.  They are dlopen'ed on the first eigendecomposition, preferring
+// the copies PyTorch itself maps (the venv's nvidia/* packages), so a process
+// that already imported torch shares their pages.
+#pragma once
+
+#include <cusolverDn.h>
+#include <dlfcn.h>
+
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace csb {
+
+struct CusolverApi {
+  void* lib = nullptr;
+  std::string path;
+  cusolverStatus_t (*create)(cusolverDnHandle_t*) = nullptr;
+  cusolverStatus_t (*destroy)(cusolverDnHandle_t) = nullptr;
+  cusolverStatus_t (*set_stream)(cusolverDnHandle_t, cudaStream_t) = nullptr;
+  cusolverStatus_t (*syevd_buffer)(cusolverDnHandle_t, cusolverEigMode_t, cublasFillMode_t, int,
+                                   const double*, int, const double*, int*) = nullptr;
+  cusolverStatus_t (*syevd)(cusolverDnHandle_t, cusolverEigMode_t, cublasFillMode_t, int, double*,
+                            int, double*, double*, int, int*) = nullptr;
+};
+
+inline const CusolverApi& cusolver_api() {
+  static CusolverApi api;
+  static std::once_flag once;
+  static std::string error;
+  std::call_once(once, [] {
+    const char* env = std::getenv("CSB_CUSOLVER");
+    const char* candidates[] = {
+        env,
+        "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cusolver/lib/libcusolver.so.11",
+        "libcusolver.so.11",
+        "/usr/local/cuda/lib64/libcusolver.so.11",
+    };
+    for (const char* c : candidates) {
+      if (!c) continue;
+      void* h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+      if (!h) {
+        error += std::string(dlerror()) + "; ";
+        continue;
+      }
+      api.lib = h;
+      api.path = c;
+      break;
+    }
+    if (!api.lib) return;
+    api.create = reinterpret_cast<decltype(api.create)>(dlsym(api.lib, "cusolverDnCreate"));
+    api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.lib, "cusolverDnDestroy"));
+    api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(api.lib, "cusolverDnSetStream"));
+    api.syevd_buffer =
+        reinterpret_cast<decltype(api.syevd_buffer)>(dlsym(api.lib, "cusolverDnDsyevd_bufferSize"));
+    api.syevd = reinterpret_cast<decltype(api.syevd)>(dlsym(api.lib, "cusolverDnDsyevd"));
+    if (!api.create || !api.destroy || !api.set_stream || !api.syevd_buffer || !api.syevd) {
+      error += "missing cuSOLVER symbols in " + api.path;
+      api.lib = nullptr;
+    }
+  });
+  if (!api.lib) fail(CS_ERROR, "symmetric_eig: cannot load cuSOLVER (" + error + ")");
+  return api;
+}
+
+}  // namespace csb

@@ -105,7 +105,12 @@ class Context:
         return buf.value.decode()
 
     def set_stream(self, stream_ptr: int | None) -> None:
-        check(_lib.lib().cs_ctx_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+        """stream_ptr: a cudaStream_t value (0 = legacy default stream);
+        None restores the context's own stream."""
+        if stream_ptr is None:
+            check(_lib.lib().cs_ctx_reset_stream(self.handle))
+        else:
+            check(_lib.lib().cs_ctx_set_stream(self.handle, C.c_void_p(stream_ptr)))
 
     def synchronize(self) -> None:
         check(_lib.lib().cs_ctx_synchronize(self.handle))

@@ -22,8 +22,11 @@ FP64_TOL = 1e-10  # test_mset.cpp:264-278 cross-backend estimate tolerance
 
 @pytest.fixture(scope="module")
 def p():
+    import torch  # noqa: F401  maps the CUDA math libraries cuSOLVER shares
     import paper_2003_08011_b200 as p
     p.context(0)  # fails loudly if the library or the device is missing
+    # one-time cold start: the first eigendecomposition binds cuSOLVER
+    p.symmetric_eig(np.eye(2), p.BackendId())
     return p
 
 

@@ -126,6 +126,16 @@ def load_traffic():
         return None
 
 
+def load_tf32_peak():
+    """Dense kind::tf32 tcgen05 throughput measured on this pool by
+    tools/mma_probe (profiles/mma_probe_tf32.json), TFLOP/s at max clock."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "mma_probe_tf32.json")))
+        return max(r["tflops_at_base_clock"] for r in d["results"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -199,6 +209,42 @@ def cpu_baseline_sample(train, obs):
             "sample": f"{CPU_SAMPLE_OBS} of {N_OBS} observations, oracle optimized backend "
                       f"(tile 64, {cores} threads) on {model_name}",
             "train_ms": train_s * 1e3}
+
+
+SWEEP_GRID = dict(signal_counts=[10, 20, 50, 100], observation_counts=[10_000, 100_000],
+                  memory_counts=[100, 200, 500, 1000])
+SWEEP_REPLICATES = 3
+
+
+def run_bench_sweep(world, rank, local, barrier, max_over_ranks):
+    """The reference's Monte Carlo scoping sweep (run_sweep, sweep.cpp:277-325)
+    on a reduced C4 grid: (cell, replicate) units LPT-placed over the ranks,
+    cost records gathered over torch.distributed.  Reports units/s over the
+    whole sweep wall time (device synthesis + timed train/estimate + gather),
+    max over ranks."""
+    from paper_2003_08011_b200 import BackendId
+    from paper_2003_08011_b200.sweep import SweepConfig, SweepGrid, SignalStatsTemplate, run_sweep
+    cfg = SweepConfig(SweepGrid(**SWEEP_GRID), replicates=SWEEP_REPLICATES, warmups=1,
+                      backends=[BackendId("b200", local, "fp32")], master_seed=MASTER_SEED,
+                      signal_template=SignalStatsTemplate(0.5, 0.3, 1.0, 0.5, 4.0))
+    barrier()
+    t0 = time.perf_counter()
+    surface = run_sweep(cfg, world=world, rank=rank, device=local)
+    barrier()
+    wall = max_over_ranks(time.perf_counter() - t0)
+    if rank != 0:
+        return None
+    units = sum(len(c.samples) for c in surface.cells if c.phase.value == "train")
+    cells = sum(1 for c in surface.cells if c.phase.value == "train" and not c.excluded)
+    excluded = sum(1 for c in surface.cells if c.phase.value == "train" and c.excluded)
+    train_s = sum(sum(c.samples) for c in surface.cells if c.phase.value == "train")
+    surv_s = sum(sum(c.samples) for c in surface.cells if c.phase.value == "surveil")
+    return {"metric": "MC sweep (cell, replicate) units/s", "value": units / wall, "unit": "units/s",
+            "cells_per_s": cells / wall, "units": units, "admissible_cells": cells,
+            "excluded_cells": excluded, "wall_s": wall, "timed_train_s": train_s,
+            "timed_surveil_s": surv_s, "scaling": "strong", "n_gpus": world,
+            "grid": {**SWEEP_GRID, "replicates": SWEEP_REPLICATES, "warmups": 1},
+            "note": "reduced C4 grid; device-side synthesis; wall includes synthesis and gather"}
 
 
 # ---------------------------------------------------------------------- B200
@@ -295,6 +341,9 @@ def run_b200(args, world, rank, local):
     # correctness guard on the e2e output: residual identity
     assert np.array_equal(res_np, obs_np - est_np)
 
+    # ---- Monte Carlo scoping sweep (cells/s), strong scaling over ranks
+    sweep = None if args.no_sweep else run_bench_sweep(world, rank, local, barrier, max_over_ranks)
+
     if rank != 0:
         return
     peaks = load_peaks()
@@ -303,7 +352,8 @@ def run_b200(args, world, rank, local):
     bf16 = peaks.get("bf16_tflops", 1590.0)
     # tensor work actually issued: 3 TF32 products per GEMM incl. padding
     K1, N2 = (N_SIG + 7) // 8 * 8, (N_SIG + 15) // 16 * 16
-    MT = 64
+    MT = 64  # tile the library selects for n = 100 (choose_tc_shape)
+    tf32_peak = load_tf32_peak() or bf16 / 2
     m_pad = (N_MEM + MT - 1) // MT * MT
     n_tiles = (N_OBS + 127) // 128
     issued = 3 * 2 * 128 * n_tiles * m_pad * (K1 + N2)
@@ -333,14 +383,19 @@ def run_b200(args, world, rank, local):
                      "frac": achieved_tflops / bf16, "traffic": traffic,
                      "kernel": "mset_estimate_tc_kernel<64,float>",
                      "algorithmic_flops_per_launch": flops_per_obs * N_OBS,
-                     "peak_note": "peak = measured dense bf16 (MEASURED_PEAKS.json); the kernel runs "
-                                  "kind::tf32 at half the bf16 rate and issues 3 products per GEMM",
-                     "peak_3xtf32_derived": bf16 / 2 / 3,
-                     "frac_3xtf32": achieved_tflops / (bf16 / 2 / 3),
+                     "peak_note": "peak = measured dense bf16 (MEASURED_PEAKS.json, of measured); the "
+                                  "kernel runs tcgen05 kind::tf32 (measured dense peak "
+                                  "peak_tf32_measured, tools/mma_probe) and issues 3 split "
+                                  "products per GEMM, so its algorithmic ceiling is peak_tf32/3",
+                     "peak_tf32_measured": tf32_peak,
+                     "peak_3xtf32": tf32_peak / 3,
+                     "frac_3xtf32": achieved_tflops / (tf32_peak / 3),
                      "issued_tf32_tflops": issued_tflops,
-                     "tensor_pipe_frac_tf32": issued_tflops / (bf16 / 2)},
+                     "tensor_pipe_frac_tf32": issued_tflops / tf32_peak},
         "clocks": clocks,
     }
+    if sweep is not None:
+        line["sweep"] = sweep
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(train, obs)
     print(json.dumps(line), flush=True)
@@ -353,6 +408,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

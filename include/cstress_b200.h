@@ -159,6 +159,13 @@ cs_status cs_model_destroy(cs_model* model);
 cs_status cs_synthesize_uniform(int64_t n, int64_t N, double phi, double rho,
                                 double variance, double skewness,
                                 double kurtosis, uint64_t seed, double* out);
+/* Same recipe on the device (d_out: column-major N x n FP64 on ctx's device):
+ * counter-based Box-Muller draws, chunked AR(1) scan, O(N n) mixing with the
+ * closed-form compound-symmetric Cholesky factor.  Tolerance parity with the
+ * host feed (libm / summation order differ in the last bits).  Synchronous. */
+cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double phi,
+                                       double rho, double variance, double skewness,
+                                       double kurtosis, uint64_t seed, double* d_out);
 uint64_t cs_derive_seed(uint64_t parent, const uint64_t* coords, int ncoords);
 /* sweep.cpp:119-126 */
 uint64_t cs_cell_data_seed(uint64_t master_seed, int64_t n_signals,

@@ -23,6 +23,7 @@
 #include "kernels_f64.cuh"
 #include "selection.cuh"
 #include "solver.cuh"
+#include "synth.cuh"
 
 using namespace csb;
 
@@ -771,6 +772,51 @@ cs_status cs_model_import(cs_ctx* ctx, int64_t n, int64_t m, int kind, double ba
     if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
     CSB_CUDA(cudaStreamSynchronize(st));
     *out = M.release();
+  });
+}
+
+cs_status csb_prepare_uniform(int64_t n, int64_t N, double phi, double rho, double variance,
+                              double skewness, double kurtosis, double fc[4]);
+}  // extern "C"
+bool csb_uniform_cholesky(int64_t n, double rho, std::vector<double>& diag, std::vector<double>& below);
+extern "C" {
+
+cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double phi, double rho,
+                                       double variance, double skewness, double kurtosis,
+                                       uint64_t seed, double* d_out) {
+  double fc[4];
+  const cs_status st0 = csb_prepare_uniform(n, N, phi, rho, variance, skewness, kurtosis, fc);
+  if (st0 != CS_OK) return st0;
+  return guarded([&] {
+    set_device(ctx->device);
+    cudaStream_t st = ctx->stream;
+    std::vector<double> diag, below;
+    const bool mix = n > 1;
+    if (mix && !csb_uniform_cholesky(n, rho, diag, below))
+      fail(CS_BAD_CORRELATION, "correlation matrix not positive semidefinite within jitter cap 1e-06");
+    const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+    DevBuf<unsigned long long> seeds(n);
+    DevBuf<double> state0(n), ends(n * chunks), carry(n * chunks), mean(n), sd(n), dg(n + 1), bl(n + 1);
+    synth_seeds_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seed, static_cast<int>(n), seeds.get());
+    synth_burnin_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), phi, state0.get());
+    synth_ar_local_kernel<<<ceil_div(n * chunks, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), N,
+                                                                      phi, d_out, ends.get());
+    synth_ar_carry_kernel<<<ceil_div(n, 128), 128, 0, st>>>(state0.get(), ends.get(), static_cast<int>(n),
+                                                             N, phi, carry.get());
+    synth_ar_apply_kernel<<<grid_for(n * N), 256, 0, st>>>(carry.get(), static_cast<int>(n), N, phi, d_out);
+    CSB_LAUNCH_CHECK();
+    col_moments_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_out, N, mean.get(), sd.get());
+    if (mix) {
+      CSB_CUDA(cudaMemcpyAsync(dg.get(), diag.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+      CSB_CUDA(cudaMemcpyAsync(bl.get(), below.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    synth_std_mix_kernel<<<ceil_div(N, 256), 256, 0, st>>>(d_out, static_cast<int>(n), N, mean.get(),
+                                                           sd.get(), dg.get(), bl.get(), mix ? 1 : 0);
+    synth_cubic_kernel<<<grid_for(n * N), 256, 0, st>>>(d_out, n * N, fc[0], fc[1], fc[2], fc[3]);
+    col_moments_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_out, N, mean.get(), sd.get());
+    synth_scale_kernel<<<grid_for(n * N), 256, 0, st>>>(d_out, static_cast<int>(n), N, sd.get(), variance);
+    CSB_LAUNCH_CHECK();
+    CSB_CUDA(cudaStreamSynchronize(st));
   });
 }
 

@@ -20,9 +20,12 @@
 
 #include "cstress_b200.h"
 
+// The C-ABI error channel lives in cstress_b200.cu; synthesis reports through
+// a setter it exports.
+extern "C" cs_status cs__set_error(cs_status code, const char* msg);
+
 namespace {
 
-thread_local std::string g_synth_error;
 
 uint64_t mix64(uint64_t z) {
   z += 0x9e3779b97f4a7c15ULL;
@@ -232,9 +235,73 @@ cs_status cs_synthesize_uniform(int64_t n, int64_t N, double phi, double rho, do
                                 double skewness, double kurtosis, uint64_t seed, double* out);
 }
 
-// The C-ABI error channel lives in cstress_b200.cu; synthesis reports through
-// a setter it exports.
-extern "C" cs_status cs__set_error(cs_status code, const char* msg);
+
+// SignalSpec::validate (signals.cpp:67-103) for a uniform spec plus the
+// Fleishman solve (signals.cpp:105-164); shared by the host and device feeds.
+extern "C" cs_status csb_prepare_uniform(int64_t n, int64_t N, double phi, double rho, double variance,
+                                         double skewness, double kurtosis, double fc[4]) {
+  if (n < 1) return cs__set_error(CS_CONFIG_ERROR, "SignalSpec: n_signals must be >= 1");
+  if (N < 1) return cs__set_error(CS_CONFIG_ERROR, "SignalSpec: n_observations must be >= 1");
+  if (!(std::fabs(phi) < 1.0))
+    return cs__set_error(CS_CONFIG_ERROR, "SignalSpec: ar_coefficient must lie in (-1, 1)");
+  if (n > 1) {
+    const double mine = std::min(1.0 - rho, 1.0 + static_cast<double>(n - 1) * rho);
+    if (mine < -1e-10)
+      return cs__set_error(CS_BAD_CORRELATION, "SignalSpec: cross_correlation has eigenvalues below -1e-10");
+  }
+  if (!(variance > 0.0)) return cs__set_error(CS_CONFIG_ERROR, "SignalSpec: variance_target must be > 0");
+  const double bound = skewness * skewness + 1.0;
+  if (!(kurtosis > bound)) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf,
+                  "SignalSpec: kurtosis_target %g for signal 0 violates the Pearson bound (must "
+                  "exceed skewness^2 + 1 = %g)",
+                  kurtosis, bound);
+    return cs__set_error(CS_MOMENT_INFEASIBLE, buf);
+  }
+  if (!fleishman(skewness, kurtosis, fc)) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "no real Fleishman solution for skewness %g, kurtosis %g", skewness,
+                  kurtosis);
+    return cs__set_error(CS_MOMENT_INFEASIBLE, buf);
+  }
+  return CS_OK;
+}
+
+// Cholesky factor of the compound-symmetric correlation matrix (unit
+// diagonal, off-diagonal rho) with the jitter ladder of nearest_psd_repair
+// (signals.cpp:166-203), in closed form: eliminating variable k leaves a
+// Schur complement that is again compound symmetric (diagonal a, off-diagonal
+// b), so L(k,k) = sqrt(a) and L(j,k) = b / sqrt(a) for every j > k.
+bool csb_uniform_cholesky(int64_t n, double rho, std::vector<double>& diag, std::vector<double>& below) {
+  std::vector<double> tried = {0.0};
+  double last = 0.0;
+  for (double j = 1e-12; j <= 1e-6; j *= 100.0) {
+    tried.push_back(j);
+    last = j;
+  }
+  if (1e-6 > last) tried.push_back(1e-6);
+  diag.assign(static_cast<size_t>(n), 0.0);
+  below.assign(static_cast<size_t>(n), 0.0);
+  for (double jit : tried) {
+    double a = 1.0, b = jit > 0.0 ? rho / (1.0 + jit) : rho;
+    bool ok = true;
+    for (int64_t k = 0; k < n; ++k) {
+      if (!(a > 0.0)) {
+        ok = false;
+        break;
+      }
+      const double l = std::sqrt(a);
+      const double c = b / l;
+      diag[k] = l;
+      below[k] = c;
+      a -= c * c;
+      b -= c * c;
+    }
+    if (ok) return true;
+  }
+  return false;
+}
 
 extern "C" cs_status cs_synthesize_uniform(int64_t n, int64_t N, double phi, double rho,
                                            double variance, double skewness, double kurtosis,

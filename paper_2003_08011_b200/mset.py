@@ -314,6 +314,23 @@ def train(training, m: int, cfg: KernelConfig = KernelConfig(),
     return TrainedModel(h, backend)
 
 
+def train_device(training, m: int, cfg: KernelConfig = KernelConfig(),
+                 backend: BackendId = BackendId()) -> TrainedModel:
+    """train on a device-resident float64 torch tensor (N x n column-major,
+    i.e. stride(0) == 1 and leading dimension N)."""
+    import torch
+    if training.dtype != torch.float64 or training.dim() != 2 or training.stride(0) != 1:
+        raise ShapeError("train_device: training must be a column-major float64 N x n tensor")
+    N, n = training.shape
+    if n > 1 and training.stride(1) != N:
+        raise ShapeError("train_device: training must be contiguous column-major (ld == N)")
+    h = C.c_void_p()
+    check(_lib.lib().cs_mset_train_device(_ctx(backend).handle, C.c_void_p(training.data_ptr()), N, n,
+                                          m, int(cfg.kind), cfg._h(), PRECISIONS[backend.precision],
+                                          C.byref(h)))
+    return TrainedModel(h, backend)
+
+
 def import_model(D, signal_scale, gram_pinv, rank, cfg: KernelConfig,
                  backend: BackendId = BackendId(), source_indices=None,
                  eigen_spectrum=None) -> TrainedModel:

@@ -54,6 +54,21 @@ def synthesize(spec: SignalSpec) -> SignalMatrix:
     return SignalMatrix(out, spec)
 
 
+def synthesize_device(spec: SignalSpec, device: int = 0):
+    """Same recipe on the GPU; returns an N x n column-major float64 torch
+    tensor on cuda:device (tolerance parity with ``synthesize``)."""
+    import torch
+    from .mset import context
+    out = torch.empty((spec.n_signals, spec.n_observations), dtype=torch.float64,
+                      device=torch.device("cuda", device)).T
+    ctx = context(device)
+    check(_lib.lib().cs_synthesize_uniform_device(
+        ctx.handle, spec.n_signals, spec.n_observations, spec.ar_coefficient,
+        spec.cross_correlation, spec.variance, spec.skewness, spec.kurtosis,
+        spec.seed & (2**64 - 1), out.data_ptr()))
+    return out
+
+
 def derive_seed(parent: int, coords) -> int:
     import ctypes as C
     arr = (C.c_uint64 * max(len(coords), 1))(*coords)

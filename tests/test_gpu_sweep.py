@@ -1,0 +1,82 @@
+"""GPU tests of the device data feed and the Monte Carlo sweep driver
+(ports of test_sweep.cpp run_cell / run_sweep cases with the B200 backend)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def p():
+    import torch  # noqa: F401
+    import paper_2003_08011_b200 as p
+    p.context(0)
+    p.symmetric_eig(np.eye(2), p.BackendId())
+    return p
+
+
+@pytest.mark.parametrize("args", [(1, 5000, 0.0, 0.0, 1.0, 0.0, 3.0, 7),
+                                  (5, 3000, 0.5, 0.3, 1.0, 0.5, 4.0, 123),
+                                  (64, 20000, 0.8, 0.9, 2.0, 1.0, 5.0, 99),
+                                  (3, 2500, -0.4, 0.2, 1.0, -0.5, 4.0, 5)])
+def test_device_synthesis_matches_host(p, args):
+    host = p.synthesize(p.SignalSpec.uniform(*args)).data
+    dev = p.synthesize_device(p.SignalSpec.uniform(*args)).cpu().numpy()
+    assert dev.shape == host.shape
+    # same recipe; libm, the AR(1) scan and the closed-form Cholesky differ
+    # from the sequential host feed only in the last bits
+    assert np.abs(dev - host).max() <= 1e-9 * np.abs(host).max()
+
+
+def test_device_synthesis_statistics(p):
+    x = p.synthesize_device(p.SignalSpec.uniform(2, 200000, 0.8, 0.9, 1.0, 0.0, 3.0, 11)).cpu().numpy()
+    assert 0.85 < np.corrcoef(x[:, 0], x[:, 1])[0, 1] < 0.95
+    c = x[:, 0] - x[:, 0].mean()
+    assert 0.75 < (c[:-1] * c[1:]).sum() / (c * c).sum() < 0.85
+
+
+def test_train_device_matches_host_train(p, oracle):
+    X = oracle.synthesize_uniform(20, 400, 0.5, 0.3, 1.0, 0.5, 4.0, 3)
+    import torch
+    d = torch.tensor(X.T.copy(), device="cuda").T
+    a = p.train_device(d, 100, p.KernelConfig(), p.BackendId()).export()
+    b = p.train(X, 100, p.KernelConfig(), p.BackendId()).export()
+    assert a["source_indices"].tolist() == b["source_indices"].tolist()
+    assert np.array_equal(a["gram_pinv"], b["gram_pinv"])
+
+
+def test_run_cell_samples_and_seeds(p):
+    from paper_2003_08011_b200.sweep import CellCoords, SweepConfig, SweepGrid, run_cell
+    from paper_2003_08011_b200 import BackendId
+    cfg = SweepConfig(SweepGrid([2], [32], [4, 8]), replicates=3, warmups=1, master_seed=1234,
+                      backends=[BackendId("b200", 0, "fp32"), BackendId("b200", 0, "fp64")])
+    cells = run_cell(CellCoords(2, 32, 4), cfg)
+    assert len(cells) == 4
+    for c in cells:
+        assert not c.excluded and len(c.samples) == 3 and all(s > 0 for s in c.samples)
+        assert c.data_seeds == cells[0].data_seeds
+    again = run_cell(CellCoords(2, 32, 4), cfg)
+    assert again[0].data_seeds == cells[0].data_seeds
+
+
+def test_run_sweep_holes_and_runtime_exclusion(p):
+    from paper_2003_08011_b200.sweep import SweepConfig, SweepGrid, run_sweep
+    cfg = SweepConfig(SweepGrid([2], [32], [2, 4]), replicates=2, warmups=0, master_seed=1234)
+    calls = []
+    s = run_sweep(cfg, lambda i, tot, c, r: calls.append(tot))
+    assert calls == [2, 2] and len(s.cells) == 4
+    assert [c.reason for c in s.cells if c.excluded] == ["m<2n", "m<2n"]
+    cfg.signal_template.skewness, cfg.signal_template.kurtosis = 2.0, 6.0
+    s = run_sweep(cfg)
+    assert all(c.excluded for c in s.cells)
+    assert all("Fleishman" in c.reason for c in s.cells if c.coords.n_memory == 4)
+
+
+def test_sweep_large_cell_runs(p):
+    # one C4-grid corner cell end to end on the device (n=100, N=1e5, m=1000)
+    from paper_2003_08011_b200.sweep import CellCoords, SweepConfig, SweepGrid, run_cell
+    cfg = SweepConfig(SweepGrid([100], [100_000], [1000]), replicates=1, warmups=0, master_seed=20260810)
+    cfg.signal_template.ar_coefficient, cfg.signal_template.cross_correlation = 0.5, 0.3
+    cfg.signal_template.skewness, cfg.signal_template.kurtosis = 0.5, 4.0
+    cells = run_cell(CellCoords(100, 100_000, 1000), cfg)
+    assert not any(c.excluded for c in cells)

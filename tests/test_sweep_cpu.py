@@ -1,0 +1,136 @@
+"""Sweep driver logic on CPU: grid walk, admissibility, aggregates, validation
+(ports of test_sweep.cpp), LPT placement, and the multi-rank gather +
+reassembly over a world_size-2 gloo group (no GPU: units are faked)."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2003_08011_b200 import errors
+from paper_2003_08011_b200.sweep import (CellCoords, CostCell, Phase, SweepConfig, SweepGrid,
+                                         generate_cells, plan_units, predicted_cost, run_sweep)
+
+
+def test_generate_cells_applies_training_constraint():
+    # test_sweep.cpp:30-46
+    cells = generate_cells(SweepGrid([32, 64], [1024], [32, 64, 128]))
+    assert len(cells) == 6
+    adm = {(c.n_signals, c.n_memory) for c, ok in cells if ok}
+    exc = {(c.n_signals, c.n_memory) for c, ok in cells if not ok}
+    assert adm == {(32, 64), (32, 128), (64, 128)}
+    assert exc == {(32, 32), (64, 32), (64, 64)}
+
+
+def test_generate_cells_order():
+    # test_sweep.cpp:48-59
+    cells = generate_cells(SweepGrid([1, 2], [10, 20], [4, 8]))
+    assert [c for c, _ in cells][:5] == [CellCoords(1, 10, 4), CellCoords(1, 20, 4), CellCoords(1, 10, 8),
+                                         CellCoords(1, 20, 8), CellCoords(2, 10, 4)]
+
+
+def test_powers_of_two_grid_and_boundary():
+    # test_sweep.cpp:61-78 / acceptance criterion 3
+    g = SweepGrid([32 << k for k in range(6)], [1024], [128 << k for k in range(7)])
+    cells = generate_cells(g)
+    assert len(cells) == 42
+    assert all(ok == (c.n_memory >= 2 * c.n_signals) for c, ok in cells)
+    assert generate_cells(SweepGrid([1], [8], [2]))[0][1]
+
+
+def test_grid_and_config_validation():
+    # test_sweep.cpp:80-89, :223-238
+    with pytest.raises(errors.ConfigError):
+        SweepGrid([], [8], [2]).validate()
+    with pytest.raises(errors.ConfigError):
+        SweepGrid([4, 4], [8], [2]).validate()
+    with pytest.raises(errors.ConfigError):
+        SweepGrid([4, 2], [8], [2]).validate()
+    g = SweepGrid([2], [32], [4, 8])
+    for bad in (dict(replicates=0), dict(backends=[]), dict(estimator="neural-net")):
+        with pytest.raises(errors.ConfigError):
+            SweepConfig(g, **bad).validate()
+    cfg = SweepConfig(g)
+    cfg.signal_template.kurtosis = 1.0
+    with pytest.raises(errors.ConfigError):
+        cfg.validate()
+
+
+def test_aggregate_arithmetic():
+    # test_sweep.cpp:205-221
+    c = CostCell(CellCoords(1, 1, 2), Phase.train, None, samples=[3.0, 1.0, 2.0])
+    c.recompute_aggregates()
+    assert c.median == 2.0 and abs(c.mean - 2.0) < 1e-12 and abs(c.stddev - 1.0) < 1e-12
+    c.samples = [4.0, 1.0, 2.0, 3.0]
+    c.recompute_aggregates()
+    assert c.median == 2.5
+    c.samples = [5.0]
+    c.recompute_aggregates()
+    assert c.median == 5.0 and c.stddev == 0.0
+
+
+def test_lpt_plan_covers_every_unit_once_and_balances():
+    cells = [c for c, ok in generate_cells(SweepGrid([10, 20, 50, 100, 200, 500, 1000],
+                                                     [10_000, 100_000, 1_000_000],
+                                                     [100, 200, 500, 1000, 2000, 4000])) if ok]
+    assert len(cells) == 96
+    units = [(i, c, r) for i, c in enumerate(cells) for r in range(5)]
+    for world in (1, 2, 4, 8):
+        plan = plan_units(units, world)
+        flat = sorted(u[:1] + u[2:] for p in plan for u in p)
+        assert flat == sorted(u[:1] + u[2:] for u in units)
+        loads = [sum(predicted_cost(u[1]) for u in p) for p in plan]
+        assert max(loads) / (sum(loads) / world) < 1.15  # near-linear 1 -> 8
+        assert plan == plan_units(units, world)           # deterministic
+
+
+def _fake_unit(coords, replicate, config, device, warm):
+    # deterministic stand-in for the timed unit (pure function of the unit)
+    rec = {"coords": (coords.n_signals, coords.n_observations, coords.n_memory),
+           "replicate": replicate, "seed": 1000 * coords.n_memory + replicate,
+           "train": [1e-3 * coords.n_memory + replicate],
+           "surveil": [1e-6 * coords.n_observations + replicate], "error": None,
+           "error_kind": None}
+    if coords.n_signals == 3 and replicate == 1:
+        rec["error"], rec["error_kind"] = "no real Fleishman solution", "MomentInfeasible"
+    return rec
+
+
+def _sweep_config():
+    return SweepConfig(SweepGrid([1, 2, 3], [16, 32], [2, 4, 8]), replicates=3, warmups=0)
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    s = run_sweep(_sweep_config(), world=world, rank=rank, unit_runner=_fake_unit)
+    if rank == 0:
+        q.put([(c.coords, c.phase.value, c.samples, c.data_seeds, c.excluded, c.reason) for c in s.cells])
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_two_rank_gloo_sweep_matches_single_rank():
+    single = run_sweep(_sweep_config(), unit_runner=_fake_unit)
+    want = [(c.coords, c.phase.value, c.samples, c.data_seeds, c.excluded, c.reason) for c in single.cells]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert got == want
+    # grid order, exclusions and per-replicate sample order survive placement
+    reasons = {r for *_, ex, r in got if ex}
+    assert reasons == {"m<2n", "no real Fleishman solution"}
+    assert len(got) == 18 * 2  # 18 grid cells x 2 phases x 1 backend

@@ -52,5 +52,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+CPP_TEST = os.path.join(ROOT, "tests", "cpp", "test_b200_api.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_b200_api")
+
+
+def build_cpp_test() -> str:
+    """The C++ host-layer test program (include/cstress_b200.hpp)."""
+    build()
+    if (os.path.exists(CPP_TEST_BIN) and os.path.getmtime(CPP_TEST_BIN) >= max(
+            os.path.getmtime(p) for p in [CPP_TEST, LIB, os.path.join(ROOT, "include", "cstress_b200.hpp")])):
+        return CPP_TEST_BIN
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), CPP_TEST,
+                    "-o", CPP_TEST_BIN, "-L", HERE, "-lcstress_b200", f"-Wl,-rpath,{HERE}"], check=True)
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

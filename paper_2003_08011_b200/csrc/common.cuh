@@ -36,6 +36,29 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define CSB_CUDA(x) ::csb::cuda_check((x), #x, __FILE__, __LINE__)
 #define CSB_LAUNCH_CHECK() ::csb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
+// Stream the C-ABI call in progress runs on (set by the entry points); device
+// buffers are allocated / freed stream-ordered on it from the device's
+// default memory pool, whose release threshold is raised so freed blocks are
+// cached instead of returned to the driver (no device-wide sync per free).
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
+inline void configure_pool(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+}
+
+struct StreamScope {  // RAII: route DevBuf traffic to `s` for one call
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~StreamScope() { alloc_stream() = prev; }
+};
+
 // Owning device buffer (grow-only when reused as workspace).
 template <typename T>
 struct DevBuf {
@@ -45,12 +68,16 @@ struct DevBuf {
   explicit DevBuf(size_t n) { resize(n); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) { o.ptr = nullptr; o.count = 0; }
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count), stream(o.stream) {
+    o.ptr = nullptr;
+    o.count = 0;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
       ptr = o.ptr;
       count = o.count;
+      stream = o.stream;
       o.ptr = nullptr;
       o.count = 0;
     }
@@ -58,7 +85,10 @@ struct DevBuf {
   }
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) {
+      if (async) cudaFreeAsync(ptr, stream);
+      else cudaFree(ptr);
+    }
     ptr = nullptr;
     count = 0;
   }
@@ -66,10 +96,28 @@ struct DevBuf {
     if (n <= count && ptr) return;
     release();
     if (n == 0) return;
-    CSB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+    if (async) {
+      stream = alloc_stream();
+      CSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), stream));
+    } else {
+      CSB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+    }
     count = n;
   }
+  cudaStream_t stream = nullptr;
+  bool async = false;  // stream-ordered pool allocation (call-local temporaries)
   T* get() const { return ptr; }
+};
+
+// Call-local temporary: allocated and freed stream-ordered on alloc_stream()
+// from the (caching) device memory pool.  Must not outlive the call's stream.
+template <typename T>
+struct TmpBuf : DevBuf<T> {
+  TmpBuf() { this->async = true; }
+  explicit TmpBuf(size_t n) {
+    this->async = true;
+    this->resize(n);
+  }
 };
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

@@ -148,10 +148,10 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
     fail(CS_INSUFFICIENT_TRAINING, buf);
   }
   // byte workspace: hashes (2N u64), keys (2N u64), rows (2N i64), flags (N), misc
-  DevBuf<unsigned long long> h1(N), h2(N);
-  DevBuf<int64_t> r1(N), r2(N), imin(n), imax(n), npicked(1);
-  DevBuf<unsigned char> selected(N);
-  DevBuf<unsigned long long> count(1);
+  TmpBuf<unsigned long long> h1(N), h2(N);
+  TmpBuf<int64_t> r1(N), r2(N), imin(n), imax(n), npicked(1);
+  TmpBuf<unsigned char> selected(N);
+  TmpBuf<unsigned long long> count(1);
   picked.resize(m);
 
   row_hash_kernel<<<ceil_div(N, 256), 256, 0, st>>>(X, N, n, h1.get());
@@ -204,7 +204,7 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
 void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
   cudaStream_t st = ctx->stream;
   if (m == 0) return;
-  DevBuf<unsigned long long> stats(2);
+  TmpBuf<unsigned long long> stats(2);
   CSB_CUDA(cudaMemsetAsync(stats.get(), 0, 2 * sizeof(unsigned long long), st));
   symmetry_stats_kernel<<<grid_for(m * m), 256, 0, st>>>(G, m, stats.get());
   CSB_LAUNCH_CHECK();
@@ -223,8 +223,8 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
   solver_check(api.syevd_buffer(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                 static_cast<int>(m), V, static_cast<int>(m), w, &lwork),
                "Dsyevd_bufferSize");
-  DevBuf<double> work(static_cast<size_t>(lwork) + 1);
-  DevBuf<int> info(1);
+  TmpBuf<double> work(static_cast<size_t>(lwork) + 1);
+  TmpBuf<int> info(1);
   solver_check(api.syevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                          static_cast<int>(m), V, static_cast<int>(m), w, work.get(), lwork, info.get()),
                "Dsyevd");
@@ -268,7 +268,7 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
   if (!M->tc) return;
   const int n = static_cast<int>(M->n), m = static_cast<int>(M->m);
   // P = D_norm * G+  (n x m), FP64, once per model
-  DevBuf<double> P(static_cast<size_t>(n) * m);
+  TmpBuf<double> P(static_cast<size_t>(n) * m);
   launch_gemm_exact<false, false>(st, M->Dn.get(), n, M->pinv.get(), m, n, m, m, P.get(), n);
   const int m_pad = M->m_tiles * M->MT;
   M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
@@ -325,7 +325,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->m = m;
   M->kind = kind;
   M->precision = precision;
-  DevBuf<int64_t> picked;
+  TmpBuf<int64_t> picked;
   trace.mark("enter");
   select_device(ctx, X, N, n, m, picked, M->source_indices);  // mset.cpp:142
   trace.mark("select_memory_vectors");
@@ -339,7 +339,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->Dn.resize(n * m);                                       // mset.cpp:147-149
   div_rows_kernel<<<grid_for(n * m), 256, 0, st>>>(M->D.get(), M->scale.get(), n, m, M->Dn.get());
   CSB_LAUNCH_CHECK();
-  DevBuf<double> gram(m * m), V(m * m);                      // mset.cpp:151-152
+  TmpBuf<double> gram(m * m), V(m * m);                      // mset.cpp:151-152
   trace.mark("scale + normalise");
   launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, kind, M->h, gram.get(), m);
   trace.mark("gram (sim_exact)");
@@ -356,7 +356,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
     if (M->spectrum_host[i] > cutoff) ++rank;
   if (rank == 0) fail(CS_DEGENERATE_MODEL, "train: all Gram eigenvalues below cutoff");
   M->rank = rank;
-  DevBuf<double> W(m * rank);                                // mset.cpp:165-170
+  TmpBuf<double> W(m * rank);                                // mset.cpp:165-170
   whiten_kernel<<<grid_for(m * rank), 256, 0, st>>>(V.get(), M->spectrum.get(), m, rank, W.get());
   CSB_LAUNCH_CHECK();
   M->pinv.resize(m * m);
@@ -502,6 +502,7 @@ cs_status cs_ctx_create(int device, cs_ctx** out) {
     if (prop.major != 10) fail(CS_ERROR, std::string("cs_ctx_create: sm_100a device required, found ") + prop.name);
     c->sm_count = prop.multiProcessorCount;
     c->name = prop.name;
+    configure_pool(device);
     CSB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking));
     CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
@@ -559,7 +560,8 @@ cs_status cs_sim_matrix(cs_ctx* ctx, const double* A, const double* B, int64_t n
     set_device(ctx->device);
     const double h = resolve_h(bandwidth, n);
     if (p == 0 || q == 0) return;
-    DevBuf<double> dA(n * p + 1), dB(n * q + 1), dO(p * q);
+    StreamScope scope(ctx->stream);
+    TmpBuf<double> dA(n * p + 1), dB(n * q + 1), dO(p * q);
     cudaStream_t st = ctx->stream;
     CSB_CUDA(cudaMemcpyAsync(dA.get(), A, n * p * sizeof(double), cudaMemcpyHostToDevice, st));
     CSB_CUDA(cudaMemcpyAsync(dB.get(), B, n * q * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -575,7 +577,8 @@ cs_status cs_matmul(cs_ctx* ctx, const double* A, const double* B, int64_t p, in
     set_device(ctx->device);
     if (p == 0 || q == 0) return;
     cudaStream_t st = ctx->stream;
-    DevBuf<double> dA(p * k + 1), dB(k * q + 1), dO(p * q);
+    StreamScope scope(ctx->stream);
+    TmpBuf<double> dA(p * k + 1), dB(k * q + 1), dO(p * q);
     CSB_CUDA(cudaMemcpyAsync(dA.get(), A, p * k * sizeof(double), cudaMemcpyHostToDevice, st));
     CSB_CUDA(cudaMemcpyAsync(dB.get(), B, k * q * sizeof(double), cudaMemcpyHostToDevice, st));
     launch_gemm_exact<false, false>(st, dA.get(), p, dB.get(), k, p, k, q, dO.get(), p);
@@ -595,7 +598,8 @@ cs_status cs_symmetric_eig(cs_ctx* ctx, const double* G, int64_t m, double* w, d
     set_device(ctx->device);
     if (m == 0) return;
     cudaStream_t st = ctx->stream;
-    DevBuf<double> dG(m * m), dV(m * m), dw(m);
+    StreamScope scope(ctx->stream);
+    TmpBuf<double> dG(m * m), dV(m * m), dw(m);
     CSB_CUDA(cudaMemcpyAsync(dG.get(), G, m * m * sizeof(double), cudaMemcpyHostToDevice, st));
     eig_device(ctx, dG.get(), m, dw.get(), dV.get());
     CSB_CUDA(cudaMemcpyAsync(w, dw.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -609,14 +613,15 @@ cs_status cs_select_memory_vectors(cs_ctx* ctx, const double* X, int64_t N, int6
   return guarded([&] {
     set_device(ctx->device);
     cudaStream_t st = ctx->stream;
-    DevBuf<double> dX(N * n + 1);
+    StreamScope scope(st);
+    TmpBuf<double> dX(N * n + 1);
     CSB_CUDA(cudaMemcpyAsync(dX.get(), X, N * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    DevBuf<int64_t> picked;
+    TmpBuf<int64_t> picked;
     std::vector<int64_t> host;
     select_device(ctx, dX.get(), N, n, m, picked, host);
     std::memcpy(idx, host.data(), m * sizeof(int64_t));
     if (D) {
-      DevBuf<double> dD(n * m);
+      TmpBuf<double> dD(n * m);
       gather_memory_kernel<<<grid_for(n * m), 256, 0, st>>>(dX.get(), N, n, picked.get(), m, dD.get());
       CSB_LAUNCH_CHECK();
       CSB_CUDA(cudaMemcpyAsync(D, dD.get(), n * m * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -630,6 +635,7 @@ cs_status cs_mset_train_device(cs_ctx* ctx, const double* dX, int64_t N, int64_t
   return guarded([&] {
     if (!out) fail(CS_CONFIG_ERROR, "cs_mset_train: null output");
     set_device(ctx->device);
+    StreamScope scope(ctx->stream);
     *out = train_device(ctx, dX, N, n, m, kind, bandwidth, precision);
   });
 }
@@ -639,7 +645,8 @@ cs_status cs_mset_train(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int6
   return guarded([&] {
     if (!out) fail(CS_CONFIG_ERROR, "cs_mset_train: null output");
     set_device(ctx->device);
-    DevBuf<double> dX(N * n + 1);
+    StreamScope scope(ctx->stream);
+    TmpBuf<double> dX(N * n + 1);
     CSB_CUDA(cudaMemcpyAsync(dX.get(), X, N * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     *out = train_device(ctx, dX.get(), N, n, m, kind, bandwidth, precision);
   });
@@ -744,6 +751,7 @@ cs_status cs_model_import(cs_ctx* ctx, int64_t n, int64_t m, int kind, double ba
     if (!out || !D || !pinv || !scale) fail(CS_CONFIG_ERROR, "cs_model_import: null argument");
     set_device(ctx->device);
     cudaStream_t st = ctx->stream;
+    StreamScope scope(st);
     std::unique_ptr<cs_model> M(new cs_model);
     M->device = ctx->device;
     M->n = n;
@@ -795,8 +803,9 @@ cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double
     if (mix && !csb_uniform_cholesky(n, rho, diag, below))
       fail(CS_BAD_CORRELATION, "correlation matrix not positive semidefinite within jitter cap 1e-06");
     const int64_t chunks = (N + kChunkT - 1) / kChunkT;
-    DevBuf<unsigned long long> seeds(n);
-    DevBuf<double> state0(n), ends(n * chunks), carry(n * chunks), mean(n), sd(n), dg(n + 1), bl(n + 1);
+    StreamScope scope(st);
+    TmpBuf<unsigned long long> seeds(n);
+    TmpBuf<double> state0(n), ends(n * chunks), carry(n * chunks), mean(n), sd(n), dg(n + 1), bl(n + 1);
     synth_seeds_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seed, static_cast<int>(n), seeds.get());
     synth_burnin_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), phi, state0.get());
     synth_ar_local_kernel<<<ceil_div(n * chunks, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), N,

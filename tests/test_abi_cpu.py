@@ -88,3 +88,13 @@ def test_algorithm_registry():
     assert p.algorithm_by_name("mean").name() == "mean"
     with pytest.raises(p.ConfigError):
         p.algorithm_by_name("svm")
+
+
+def test_cpp_host_layer_compiles_and_links():
+    """include/cstress_b200.hpp (C++ mirror of the reference API) builds
+    against the library; the test program lists its cases without a GPU."""
+    import subprocess
+    from paper_2003_08011_b200 import build as b
+    exe = b.build_cpp_test()
+    out = subprocess.run([exe, "--list"], capture_output=True, text=True, check=True).stdout
+    assert "train / estimate" in out and "plugin contract" in out

@@ -332,3 +332,12 @@ def test_c2_full_size_fp32_properties(p, oracle):
     o = oracle.train(X, 1000, 0, backend=oracle.OPTIMIZED, tile=64, workers=8)
     want = oracle.estimate(o, obs[sel], oracle.OPTIMIZED, 64, 8)[0]
     assert rel(r.estimates[sel], want) <= FP32_TOL
+
+
+def test_cpp_host_layer_on_gpu(p):
+    """C++ ports of test_mset.cpp / test_backends.cpp through the C++ host layer."""
+    import subprocess
+    from paper_2003_08011_b200 import build as b
+    r = subprocess.run([b.build_cpp_test()], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

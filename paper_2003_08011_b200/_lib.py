@@ -15,6 +15,9 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcstress_b200.so")
+# development tools (tools/timeline.py) may point at an instrumented build
+if os.environ.get("CSB_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["CSB_LIB"])
 
 _lib = None
 

@@ -93,6 +93,7 @@ struct cs_model {
   bool tc = false;
   int MT = 0, NB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
   DevBuf<float> dn_tiles, p_tiles, dd, dn32, inv_scale, scale_f;
+  float dd_max = 0.f;  // max ||D_norm(:, i)||^2 (near-zero guard prefilter)
 };
 
 namespace {
@@ -236,7 +237,7 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
 
 // ------------------------------------------------------ FP32 operand packing
 void choose_tc_shape(cs_model* M) {
-  M->K1 = static_cast<int>((M->n + 7) / 8 * 8);
+  M->K1 = static_cast<int>((M->n + 1 + 7) / 8 * 8);  // + the ||d||^2 column
   M->N2 = static_cast<int>((M->n + 15) / 16 * 16);
   M->MT = 0;
   // (memory tile MT, TMEM buffers NB) in order of preference.  A TS-form
@@ -287,7 +288,11 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
       M->Dn.get(), M->scale.get(), n, m, m_pad, M->dd.get(), M->dn32.get(), M->inv_scale.get(),
       M->scale_f.get());
   CSB_LAUNCH_CHECK();
+  std::vector<float> dd_host(m_pad);
+  CSB_CUDA(cudaMemcpyAsync(dd_host.data(), M->dd.get(), m_pad * sizeof(float), cudaMemcpyDeviceToHost, st));
   CSB_CUDA(cudaStreamSynchronize(st));  // P is freed on return
+  M->dd_max = 0.f;
+  for (float v : dd_host) M->dd_max = std::max(M->dd_max, v);
 }
 
 // ----------------------------------------------------------------- train
@@ -429,6 +434,7 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   p.inv_h = static_cast<float>(1.0 / M->h);
   p.g_coef = static_cast<float>(1.4426950408889634 / (2.0 * M->h * M->h));
   p.tau = 1.0f / 128.0f;
+  p.dd_max = M->dd_max;
   p.est = est;
   p.resid = resid;
   p.dn_stage_bytes = static_cast<uint32_t>(2 * M->MT * M->K1 * 4);
@@ -438,11 +444,27 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
                       tc_aux_bytes(p.K1);
   const int tiles = static_cast<int>((N + kObsTile - 1) / kObsTile);
   const int grid = std::min(tiles, ctx->sm_count);
+#ifdef CSB_TIMELINE
+  TmpBuf<unsigned long long> tl(static_cast<size_t>(4) * kTlCap * 2);
+  CSB_CUDA(cudaMemsetAsync(tl.get(), 0, 4 * kTlCap * 2 * 8, st));
+  p.timeline = tl.get();
+#endif
   auto go = [&](auto kernel) {
     CSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     kernel<<<grid, kTcThreads, smem, st>>>(p);
     CSB_LAUNCH_CHECK();
+#ifdef CSB_TIMELINE
+    std::vector<unsigned long long> h(static_cast<size_t>(4) * kTlCap * 2);
+    CSB_CUDA(cudaMemcpyAsync(h.data(), tl.get(), h.size() * 8, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    if (const char* out = std::getenv("CSB_TIMELINE_OUT")) {
+      if (FILE* f = std::fopen(out, "wb")) {
+        std::fwrite(h.data(), 8, h.size(), f);
+        std::fclose(f);
+      }
+    }
+#endif
   };
   switch (M->MT * 10 + M->NB) {
     case 1282: go(mset_estimate_tc_kernel<128, 2, IO>); break;

@@ -61,10 +61,34 @@ struct TcParams {
   float inv_h;   // 1/h            (inverse distance)
   float g_coef;  // log2(e)/(2h^2) (gaussian)
   float tau;     // near-zero recompute threshold
+  float dd_max;  // max ||d_i||^2: per-row prefilter bound for the guard
   void* est;
   void* resid;
   uint32_t dn_stage_bytes, p_stage_bytes;
+  unsigned long long* timeline;  // CSB_TIMELINE builds only: per-warp event records
 };
+
+// Development instrumentation (tools/timeline.py): with -DCSB_TIMELINE the
+// producer, MMA and two epilogue warps of CTA 0 record (event, step, clock64)
+// triples; compiled out otherwise.
+#ifdef CSB_TIMELINE
+constexpr int kTlCap = 8192;
+#define CSB_TL(slot, ev, j)                                                                   \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && lane == 0 && p.timeline) {                                       \
+      unsigned long long* tl_ = p.timeline + (slot) * kTlCap * 2;                             \
+      const unsigned long long k_ = tl_[0]++;                                               \
+      if (k_ + 1 < kTlCap) {                                                                \
+        tl_[2 + 2 * k_] = (static_cast<unsigned long long>(ev) << 32) | static_cast<unsigned>(j); \
+        tl_[3 + 2 * k_] = clock64();                                                        \
+      }                                                                                     \
+    }                                                                                       \
+  } while (0)
+#else
+#define CSB_TL(slot, ev, j) \
+  do {                      \
+  } while (0)
+#endif
 
 // TMEM columns used for a given shape and buffer count NB (1 or 2).
 __host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB) {
@@ -101,8 +125,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
   constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
   static_assert(COLS % 8 == 0, "epilogue column slice must be a multiple of 8");
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index via shfl: the compiler then knows every role branch is
+  // warp-uniform and keeps the MMA issue loop on the uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / 32, 0);
+  const int lane = threadIdx.x % 32;
   const int NS = p.n_stages;
+  constexpr int io_bytes = sizeof(IO);
   uint8_t* dn_ring = smem;
   uint8_t* p_ring = smem + NS * p.dn_stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(p_ring + NS * p.p_stage_bytes);
@@ -150,7 +178,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
+  // The CTA owns all 512 TMEM columns (1 CTA/SM), so the allocation always
+  // starts at lane 0, column 0.  Using the constant (checked) keeps every
+  // TMEM operand of the MMA issue loop in uniform registers; an address
+  // loaded from shared memory is per-thread to the compiler and turns each
+  // tcgen05.mma into an R2UR/VOTEU waterfall.
+  if (*tmem_holder != 0u) __trap();
+  constexpr uint32_t tmem = 0;
 
   const int K1 = p.K1, N2 = p.N2;
   const uint32_t colO = 0;
@@ -166,13 +200,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
     {
       Ring r(NS);
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        // warm L2 with the next tile's observations (one 128-row segment per
+        // signal column): the x prologue then reads L2, not a DRAM burst
+        // that every CTA issues at the same moment
+        const int nt = tile + gridDim.x;
+        if (nt < n_tiles) {
+          const int64_t t0 = static_cast<int64_t>(nt) * kObsTile;
+          const int64_t rows = min(static_cast<int64_t>(kObsTile), p.N - t0);
+          const uintptr_t base = reinterpret_cast<uintptr_t>(p.obs);
+          for (int s = lane; s < p.n; s += 32) {
+            const uintptr_t a = base + static_cast<uintptr_t>(t0 + static_cast<int64_t>(s) * p.ld) * io_bytes;
+            const uintptr_t a0 = a & ~uintptr_t{15}, a1 = (a + rows * io_bytes) & ~uintptr_t{15};
+            if (a1 > a0) ptx::prefetch_l2(reinterpret_cast<const void*>(a0), static_cast<uint32_t>(a1 - a0));
+          }
+        }
         for (int j = 0; j < T; ++j, r.next()) {
+          CSB_TL(0, 30, j);
           ptx::mbar_wait(&dn_empty[r.idx], r.phase ^ 1);
+          CSB_TL(0, 31, j);
           ptx::mbar_arrive_expect_tx_elect(&dn_full[r.idx], p.dn_stage_bytes);
           ptx::bulk_g2s_elect(dn_ring + r.idx * p.dn_stage_bytes,
                               p.dn_tiles + static_cast<size_t>(j) * (p.dn_stage_bytes / 4),
                               p.dn_stage_bytes, &dn_full[r.idx]);
           ptx::mbar_wait(&p_empty[r.idx], r.phase ^ 1);
+          CSB_TL(0, 33, j);
           ptx::mbar_arrive_expect_tx_elect(&p_full[r.idx], p.p_stage_bytes);
           ptx::bulk_g2s_elect(p_ring + r.idx * p.p_stage_bytes,
                               p.p_tiles + static_cast<size_t>(j) * (p.p_stage_bytes / 4),
@@ -202,10 +253,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
 
       auto issue_g1 = [&](int j) {
         const int b = NB == 2 ? (j & 1) : 0;
+        CSB_TL(1, 1, j);
         if (j == 0) ptx::mbar_wait(x_ready, tcount1 & 1);
         ptx::mbar_wait(&dn_full[rd.idx], rd.phase);
         ptx::mbar_wait(&acc_free[b], (acc_use[b] & 1) ^ 1);
         ptx::tc_fence_after();
+        CSB_TL(1, 2, j);
         const uint32_t dS = tmem + colAcc + b * MT;
         uint64_t bh = dn_desc0 + rd.idx * dn_stage_off;
         uint64_t bl = bh + dn_lo_off;
@@ -230,10 +283,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       };
       auto issue_g2 = [&](int j) {
         const int b = NB == 2 ? (j & 1) : 0;
+        CSB_TL(1, 3, j);
         ptx::mbar_wait(&s_ready[b], s_use[b] & 1);
         ptx::mbar_wait(&p_full[rp.idx], rp.phase);
         if (j == 0) ptx::mbar_wait(o_free, (tcount2 & 1) ^ 1);
         ptx::tc_fence_after();
+        CSB_TL(1, 4, j);
         const uint64_t bh0 = p_desc0 + rp.idx * p_stage_off;
         const uint64_t bl0 = bh0 + p_lo_off;
         uint32_t ah = tmem + colS + b * 2 * MT;
@@ -284,7 +339,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
     const bool gaussian = p.kind == CS_KERNEL_GAUSSIAN;
     const int c0 = half * COLS;
 
-    // normalised observation value (branch-free: out-of-range reads element 0)
+    // normalised observation value (branch-free: out-of-range reads element
+    // 0); column n is the constant 1 that multiplies the ||d||^2 column of
+    // the packed D_norm^T tiles.
     auto xnorm = [&](int64_t t, int s, bool valid) -> float {
       const bool ok = valid && s < p.n;
       const IO raw = obs[ok ? t + static_cast<int64_t>(s) * p.ld : 0];
@@ -294,38 +351,88 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       } else {
         v = static_cast<float>(raw) * s_inv_f[s];
       }
-      return ok ? v : 0.f;
+      return ok ? v : (s == p.n ? 1.f : 0.f);
+    };
+
+    // raw observations of row t, signals 8 c .. 8 c + 7 (rows past N read
+    // row 0, signals past n read signal n-1; callers mask both)
+    auto load_chunk = [&](int64_t t, bool valid, int c, IO* r) {
+      const int64_t tt = valid ? t : 0;
+      if ((c + 1) * 8 <= p.n) {
+        ptx::ldg8_strided(obs + tt + static_cast<int64_t>(c) * 8 * p.ld, p.ld, r);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[e] = obs[tt + static_cast<int64_t>(min(c * 8 + e, p.n - 1)) * p.ld];
+      }
+    };
+    // normalise a raw value of signal s (column n is the constant 1)
+    auto norm = [&](IO raw, int s, bool valid) -> float {
+      float v;
+      if constexpr (sizeof(IO) == 8) {
+        v = static_cast<float>(static_cast<double>(raw) * s_inv_d[s]);
+      } else {
+        v = static_cast<float>(raw) * s_inv_f[s];
+      }
+      return (valid && s < p.n) ? v : (s == p.n ? 1.f : 0.f);
     };
 
     uint32_t prologue_count = 0;
     // x prologue: warp group g4 normalises, splits and stores K-chunks
-    // k8 = g4 mod 4 and contributes a partial ||x||^2 for its chunks.
+    // k8 = g4 mod 4 and contributes a partial ||x||^2 for its chunks.  All
+    // loads of a batch are issued before any is consumed (one HBM latency
+    // per batch instead of one per chunk).
+    constexpr int PB = sizeof(IO) == 8 ? 2 : 4;  // chunks per load batch
     auto prologue = [&](int tile) {
-      ptx::mbar_wait(x_free, (prologue_count & 1) ^ 1);
-      ++prologue_count;
-      ptx::tc_fence_after();
+      CSB_TL(2 + (ew >> 3), 20, tile);
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
       float acc = 0.f;
-      for (int k8 = g4; k8 < K1 / 8; k8 += 4) {
-        float xv[8];
+      bool waited = false;
+      for (int k0 = g4; k0 < K1 / 8; k0 += 4 * PB) {
+        float xv[PB][8];
+        {
+          IO raw[PB][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) xv[e] = xnorm(t, k8 * 8 + e, valid);
-        uint32_t hi[8], lo[8];
+          for (int b = 0; b < PB; ++b)
+            if (k0 + 4 * b < K1 / 8) load_chunk(t, valid, min(k0 + 4 * b, (p.n - 1) / 8), raw[b]);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          acc = fmaf(xv[e], xv[e], acc);
-          const uint32_t h = ptx::to_tf32(xv[e]);
-          hi[e] = h;
-          lo[e] = __float_as_uint(xv[e] - __uint_as_float(h));
+          for (int b = 0; b < PB; ++b)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) xv[b][e] = norm(raw[b][e], (k0 + 4 * b) * 8 + e, valid);
         }
-        ptx::tmem_st8(tmem + lane_off + colXh + k8 * 8, hi);
-        ptx::tmem_st8(tmem + lane_off + colXl + k8 * 8, lo);
+        if (!waited) {
+          ptx::mbar_wait(x_free, (prologue_count & 1) ^ 1);
+          ++prologue_count;
+          ptx::tc_fence_after();
+          CSB_TL(2 + (ew >> 3), 21, tile);
+          waited = true;
+        }
+#pragma unroll
+        for (int b = 0; b < PB; ++b) {
+          const int k8 = k0 + 4 * b;
+          if (k8 >= K1 / 8) break;
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (k8 * 8 + e < p.n) acc = fmaf(xv[b][e], xv[b][e], acc);
+            const uint32_t h = ptx::to_tf32(xv[b][e]);
+            hi[e] = h;
+            lo[e] = __float_as_uint(xv[b][e] - __uint_as_float(h));
+          }
+          ptx::tmem_st8(tmem + lane_off + colXh + k8 * 8, hi);
+          ptx::tmem_st8(tmem + lane_off + colXl + k8 * 8, lo);
+        }
+      }
+      if (!waited) {
+        ptx::mbar_wait(x_free, (prologue_count & 1) ^ 1);
+        ++prologue_count;
+        ptx::tc_fence_after();
       }
       s_xx[g4 * kObsTile + row] = acc;
       ptx::tc_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
+      CSB_TL(2 + (ew >> 3), 22, tile);
       if (lane == 0) ptx::mbar_arrive(x_ready);
     };
     auto gather_xx = [&]() -> float {
@@ -338,10 +445,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
     };
 
     uint32_t use = 0, tcount = 0;  // uses of this set's TMEM buffers
-    float xx_cur = 0.f;
+    float xx_cur = 0.f, thr_cur = 0.f;
+    auto set_thr = [&]() { thr_cur = p.tau * p.dd_max - (1.f - p.tau) * xx_cur; };
     if (static_cast<int>(blockIdx.x) < n_tiles) {
       prologue(blockIdx.x);
       xx_cur = gather_xx();
+      set_thr();
     }
     const uint32_t a_base = colAcc + set * MT + c0;
     const uint32_t s_base = colS + set * 2 * MT + c0;
@@ -358,33 +467,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
           } else {
             ptx::tmem_ld8_wait(tmem + lane_off + a_base + c * CH, v);
           }
-          float ddv[CH];
-#pragma unroll
-          for (int e = 0; e < CH / 4; ++e) {
-            const float4 w = __ldg(reinterpret_cast<const float4*>(dd + c * CH) + e);
-            ddv[4 * e] = w.x;
-            ddv[4 * e + 1] = w.y;
-            ddv[4 * e + 2] = w.z;
-            ddv[4 * e + 3] = w.w;
-          }
-          // d2 in GEMM form; track the smallest margin to the cancellation guard
-          float margin = 1.f;
+          // ACC = ||d||^2 - 2 x.d (tensor core); d2 = ACC + ||x||^2.  The
+          // prefilter min(ACC) < thr is a superset of the exact near-zero
+          // criterion d2 < tau (||x||^2 + ||d||^2), re-checked per entry.
+          float mn = v[0];
 #pragma unroll
           for (int e = 0; e < CH; ++e) {
-            const float base = xx_cur + ddv[e];
-            const float d2 = fmaf(-2.f, v[e], base);
-            margin = fminf(margin, fmaf(-p.tau, base, d2));
-            v[e] = d2;
+            mn = fminf(mn, v[e]);
+            v[e] += xx_cur;
           }
-          if (margin < 0.f && valid) {  // rare: direct difference, not unrolled
+          if (mn < thr_cur && valid) {  // rare: direct difference, not unrolled
 #pragma unroll 1
             for (int e = 0; e < CH; ++e) {
-              float base = 0.f, cur = 0.f;
+              float cur = 0.f;
 #pragma unroll
               for (int ee = 0; ee < CH; ++ee)
-                if (ee == e) { base = xx_cur + ddv[ee]; cur = v[ee]; }
+                if (ee == e) cur = v[ee];
               const int col = c * CH + e;
-              if (col >= valid_cols || !(cur < p.tau * base)) continue;
+              if (col >= valid_cols || !(cur < p.tau * (xx_cur + __ldg(dd + col)))) continue;
               const int mem = j * MT + c0 + col;
               float a = 0.f;
               for (int s = 0; s < p.n; ++s) {
@@ -400,11 +500,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
 #pragma unroll
             for (int e = 0; e < CH; ++e) v[e] = ptx::ex2_approx(-fmaxf(v[e], 0.f) * p.g_coef);
           } else {
+            // 1 / (1 + sqrt(d2)/h): sqrt on the MUFU pipe; the reciprocal
+            // alternates between MUFU and an FMA-pipe Newton iteration so the
+            // two pipes share the work.
 #pragma unroll
             for (int e = 0; e < CH; ++e) {
-              const float d2 = fmaxf(v[e], 1e-30f);
-              const float r = d2 * ptx::rsqrt_approx(d2);
-              v[e] = ptx::rcp_approx(fmaf(r, p.inv_h, 1.f));
+              const float x = fmaf(ptx::sqrt_approx(fmaxf(v[e], 0.f)), p.inv_h, 1.f);
+              v[e] = (e & 1) ? ptx::rcp_newton(x) : ptx::rcp_approx(x);
             }
           }
           if (valid_cols < (c + 1) * CH) {
@@ -429,8 +531,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
             ptx::tmem_st8(tmem + lane_off + s_base + MT + c * CH + h8 * 8, lo);
           }
         };
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 10, j);
         ptx::mbar_wait(&acc_full[set], use & 1);
         ptx::tc_fence_after();
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 11, j);
         if constexpr (NB == 1) {
           // single buffers: release ACC as early as possible (GEMM1 of the
           // next step may start), then wait for GEMM2 of the previous step
@@ -441,8 +545,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
+          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
           ptx::mbar_wait(&s_free[set], (use & 1) ^ 1);
           ptx::tc_fence_after();
+          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 13, j);
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) store_chunk(c, vall + c * CH);
         } else {
@@ -462,39 +568,64 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         ptx::tc_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 14, j);
         if (lane == 0) ptx::mbar_arrive(&s_ready[set]);
       }
       // next tile's x prologue overlaps this tile's last GEMM2
       const int next = tile + gridDim.x;
       if (next < n_tiles) prologue(next);
 
-      // readout: estimate = scale .* O, residual = x - estimate
-      ptx::mbar_wait(o_full, tcount & 1);
-      ptx::tc_fence_after();
-      for (int c = g4; c < N2 / 8; c += 4) {
-        float o[8];
-        ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+      // readout: estimate = scale .* O, residual = x - estimate.  The raw
+      // observations of a batch are loaded before waiting for O.
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
+      bool o_ready = false;
+      for (int cb = g4; cb < N2 / 8; cb += 4 * PB) {
+        IO xr[PB][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int s = c * 8 + e;
-          const bool ok = valid && s < p.n;
-          const int64_t idx = ok ? t + static_cast<int64_t>(s) * p.ld : 0;
-          const IO x = obs[idx];
-          if constexpr (sizeof(IO) == 8) {
-            const double ev = static_cast<double>(o[e]) * s_scale_d[s];
-            if (ok && est) est[idx] = ev;
-            if (ok && resid) resid[idx] = x - ev;
-          } else {
-            const float ev = o[e] * s_scale_f[s];
-            if (ok && est) est[idx] = ev;
-            if (ok && resid) resid[idx] = x - ev;
+        for (int b = 0; b < PB; ++b)
+          if (cb + 4 * b < N2 / 8) load_chunk(t, valid, min(cb + 4 * b, (p.n - 1) / 8), xr[b]);
+        if (!o_ready) {
+          ptx::mbar_wait(o_full, tcount & 1);
+          ptx::tc_fence_after();
+          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
+          o_ready = true;
+        }
+#pragma unroll
+        for (int b = 0; b < PB; ++b) {
+          const int c = cb + 4 * b;
+          if (c >= N2 / 8) break;
+          float o[8];
+          ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int s = c * 8 + e;
+            const bool ok = valid && s < p.n;
+            const int64_t idx = t + static_cast<int64_t>(s) * p.ld;
+            if constexpr (sizeof(IO) == 8) {
+              const double ev = static_cast<double>(o[e]) * s_scale_d[s];
+              if (ok && est) est[idx] = ev;
+              if (ok && resid) resid[idx] = xr[b][e] - ev;
+            } else {
+              const float ev = o[e] * s_scale_f[s];
+              if (ok && est) est[idx] = ev;
+              if (ok && resid) resid[idx] = xr[b][e] - ev;
+            }
           }
         }
+      }
+      if (!o_ready) {
+        ptx::mbar_wait(o_full, tcount & 1);
+        ptx::tc_fence_after();
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(o_free);
-      if (next < n_tiles) xx_cur = gather_xx();
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
+      if (next < n_tiles) {
+        xx_cur = gather_xx();
+        set_thr();
+      }
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 26, tile);
     }
   }
   __syncthreads();

@@ -12,7 +12,10 @@ __device__ __forceinline__ size_t canon_off(int r, int k, int R) {
   return static_cast<size_t>((r & 7) * 4 + (r >> 3) * 32 + (k & 3) + (k >> 2) * (R / 8) * 32);
 }
 
-// D_norm^T tiles: block j holds memory vectors j*MT.. as rows, signals as K.
+// D_norm^T tiles: block j holds memory vectors j*MT.. as rows, signals as K,
+// pre-scaled for the GEMM-form distance: column k < n holds -2 d_k (exact),
+// column n holds ||d||^2 (FP64, split) -- with x augmented by a constant 1 in
+// column n, GEMM1 yields ||d||^2 - 2 x.d directly (one FADD of ||x||^2 left).
 __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m, int MT, int K1,
                                      int m_tiles, float* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(MT) * K1;
@@ -23,7 +26,17 @@ __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m
     const int rem = static_cast<int>(e % per);
     const int r = rem % MT, k = rem / MT;
     const int mem = j * MT + r;
-    const double v = (k < n && mem < m) ? Dn[k + static_cast<int64_t>(mem) * n] : 0.0;
+    double v = 0.0;
+    if (mem < m) {
+      if (k < n) {
+        v = -2.0 * Dn[k + static_cast<int64_t>(mem) * n];
+      } else if (k == n) {
+        for (int s = 0; s < n; ++s) {
+          const double d = Dn[s + static_cast<int64_t>(mem) * n];
+          v = fma(d, d, v);
+        }
+      }
+    }
     const float f = static_cast<float>(v);
     const float hi = __uint_as_float(ptx::to_tf32(f));
     const float lo = static_cast<float>(v - static_cast<double>(hi));

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "estimate_tc.cuh"
+#include "gemm_tc.cuh"
 #include "kernels_f64.cuh"
 #include "selection.cuh"
 #include "solver.cuh"
@@ -78,6 +79,7 @@ struct cs_ctx {
   DevBuf<double> wsA, wsB, wsC, wsD;
   DevBuf<double> io_in[2], io_est[2], io_res[2];
   DevBuf<unsigned char> wsBytes;
+  DevBuf<float> wsX[2], wsS[2], wsXX[2];  // large-n surveillance (per stream slot): x, S operands, ||x||^2
 };
 
 struct cs_model {
@@ -94,6 +96,11 @@ struct cs_model {
   int MT = 0, NB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
   DevBuf<float> dn_tiles, p_tiles, dd, dn32, inv_scale, scale_f;
   float dd_max = 0.f;  // max ||D_norm(:, i)||^2 (near-zero guard prefilter)
+  // large-n two-GEMM path (gemm_tc.cuh), used when the fused kernel's TMEM
+  // plan does not fit (n > ~130)
+  bool gemm = false;
+  int bnA = 256, ntA = 0, kcA = 0, bnB = 256, ntB = 0, kcB = 0;
+  DevBuf<float> dn_gemm, p_gemm;
 };
 
 namespace {
@@ -266,24 +273,49 @@ void choose_tc_shape(cs_model* M) {
 void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
   cudaStream_t st = ctx->stream;
   choose_tc_shape(M);
-  if (!M->tc) return;
   const int n = static_cast<int>(M->n), m = static_cast<int>(M->m);
+  int m_pad = 0;
+  if (M->tc) {
+    m_pad = M->m_tiles * M->MT;
+  } else {
+    // two-GEMM path: GEMM-A N = memory vectors, GEMM-B N = signals
+    M->gemm = true;
+    M->bnA = m >= 256 ? 256 : 128;
+    M->ntA = (m + M->bnA - 1) / M->bnA;
+    m_pad = M->ntA * M->bnA;
+    M->kcA = (n + 1 + kGemmBK - 1) / kGemmBK;
+    M->bnB = n > 128 ? 256 : 128;
+    M->ntB = (n + M->bnB - 1) / M->bnB;
+    M->kcB = m_pad / kGemmBK;
+  }
   // P = D_norm * G+  (n x m), FP64, once per model
   TmpBuf<double> P(static_cast<size_t>(n) * m);
   launch_gemm_exact<false, false>(st, M->Dn.get(), n, M->pinv.get(), m, n, m, m, P.get(), n);
-  const int m_pad = M->m_tiles * M->MT;
-  M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
-  M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
+  if (M->tc) {
+    M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
+    M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
+    pack_dn_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->K1), 256, 0, st>>>(
+        M->Dn.get(), n, m, M->MT, M->K1, M->m_tiles, M->dn_tiles.get());
+    CSB_LAUNCH_CHECK();
+    pack_p_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->N2), 256, 0, st>>>(
+        P.get(), n, m, M->MT, M->N2, M->m_tiles, M->p_tiles.get());
+    CSB_LAUNCH_CHECK();
+  } else {
+    const size_t a_el = static_cast<size_t>(M->ntA) * M->kcA * gemm_block_floats(M->bnA);
+    const size_t b_el = static_cast<size_t>(M->ntB) * M->kcB * gemm_block_floats(M->bnB);
+    M->dn_gemm.resize(a_el);
+    M->p_gemm.resize(b_el);
+    pack_dn_gemm_kernel<<<grid_for(static_cast<int64_t>(a_el / 2)), 256, 0, st>>>(
+        M->Dn.get(), n, m, M->bnA, M->ntA, M->kcA, M->dn_gemm.get());
+    CSB_LAUNCH_CHECK();
+    pack_p_gemm_kernel<<<grid_for(static_cast<int64_t>(b_el / 2)), 256, 0, st>>>(
+        P.get(), n, m, M->bnB, M->ntB, M->kcB, M->p_gemm.get());
+    CSB_LAUNCH_CHECK();
+  }
   M->dd.resize(m_pad);
   M->dn32.resize(static_cast<size_t>(n) * m);
   M->inv_scale.resize(n);
   M->scale_f.resize(n);
-  pack_dn_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->K1), 256, 0, st>>>(
-      M->Dn.get(), n, m, M->MT, M->K1, M->m_tiles, M->dn_tiles.get());
-  CSB_LAUNCH_CHECK();
-  pack_p_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->N2), 256, 0, st>>>(
-      P.get(), n, m, M->MT, M->N2, M->m_tiles, M->p_tiles.get());
-  CSB_LAUNCH_CHECK();
   pack_aux_kernel<<<grid_for(std::max<int64_t>(m_pad, static_cast<int64_t>(n) * m)), 256, 0, st>>>(
       M->Dn.get(), M->scale.get(), n, m, m_pad, M->dd.get(), M->dn32.get(), M->inv_scale.get(),
       M->scale_f.get());
@@ -478,8 +510,81 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   }
 }
 
+// Large-n surveillance: per observation block, pack x -> GEMM-A (similarity
+// epilogue writes S operand blocks) -> GEMM-B (estimate / residual epilogue).
+template <int BN, class Epi>
+void launch_gemm3x(cs_ctx* ctx, cudaStream_t st, const GemmShape& g, const Epi& epi) {
+  const int tiles = g.m_tiles * g.n_tiles;
+  if (tiles == 0) return;
+  const size_t smem = gemm3x_smem_bytes<BN>();
+  auto kernel = gemm3x_tf32_kernel<BN, Epi>;
+  CSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kernel<<<std::min(tiles, ctx->sm_count), kGemmThreads, smem, st>>>(g, epi);
+  CSB_LAUNCH_CHECK();
+}
+
+template <typename IO>
+void estimate_gemm(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, int64_t N, int64_t ld,
+                   IO* est, IO* resid, int slot = 0) {
+  if (N == 0) return;
+  const int n = static_cast<int>(M->n), m = static_cast<int>(M->m);
+  const int64_t m_pad = static_cast<int64_t>(M->ntA) * M->bnA;
+  // block size: S operand (8 bytes per observation x memory vector) <= 1 GiB
+  int64_t Nb = std::max<int64_t>(kGemmBM, ((int64_t{1} << 30) / (m_pad * 8)) / kGemmBM * kGemmBM);
+  Nb = std::min<int64_t>(Nb, (N + kGemmBM - 1) / kGemmBM * kGemmBM);
+  ctx->wsX[slot].resize(static_cast<size_t>(Nb) * M->kcA * kGemmBK * 2);
+  ctx->wsS[slot].resize(static_cast<size_t>(Nb) * m_pad * 2);
+  ctx->wsXX[slot].resize(Nb);
+  for (int64_t t0 = 0; t0 < N; t0 += Nb) {
+    const int64_t nc = std::min(Nb, N - t0);
+    const int mt = static_cast<int>((nc + kGemmBM - 1) / kGemmBM);
+    pack_obs_kernel<IO><<<grid_for(static_cast<int64_t>(mt) * kGemmBM * M->kcA * kGemmBK / 4), 256, 0, st>>>(
+        obs + t0, nc, ld, n, M->scale.get(), M->inv_scale.get(), M->kcA, ctx->wsX[slot].get(), nullptr);
+    CSB_LAUNCH_CHECK();
+    obs_sqnorm_kernel<IO><<<grid_for(nc), 256, 0, st>>>(obs + t0, nc, ld, n, M->scale.get(),
+                                                         M->inv_scale.get(), ctx->wsXX[slot].get());
+    CSB_LAUNCH_CHECK();
+    EpiSim es{};
+    es.s_tiles = ctx->wsS[slot].get();
+    es.s_k_chunks = M->kcB;
+    es.xx = ctx->wsXX[slot].get();
+    es.dd = M->dd.get();
+    es.dn32 = M->dn32.get();
+    es.obs = obs + t0;
+    es.inv_scale_f = M->inv_scale.get();
+    es.scale_d = M->scale.get();
+    es.io_f64 = sizeof(IO) == 8;
+    es.N = nc;
+    es.ld = ld;
+    es.n = n;
+    es.m = m;
+    es.kind = M->kind;
+    es.inv_h = static_cast<float>(1.0 / M->h);
+    es.g_coef = static_cast<float>(1.4426950408889634 / (2.0 * M->h * M->h));
+    es.tau = 1.0f / 128.0f;
+    es.dd_max = M->dd_max;
+    const GemmShape ga{ctx->wsX[slot].get(), M->dn_gemm.get(), mt, M->ntA, M->kcA};
+    if (M->bnA == 256) launch_gemm3x<256>(ctx, st, ga, es);
+    else launch_gemm3x<128>(ctx, st, ga, es);
+    EpiOut<IO> eo{obs + t0, est ? est + t0 : nullptr, resid ? resid + t0 : nullptr, M->scale_f.get(),
+                  M->scale.get(), nc, ld, n};
+    const GemmShape gb{ctx->wsS[slot].get(), M->p_gemm.get(), mt, M->ntB, M->kcB};
+    if (M->bnB == 256) launch_gemm3x<256>(ctx, st, gb, eo);
+    else launch_gemm3x<128>(ctx, st, gb, eo);
+  }
+}
+
 void estimate_device_any(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const void* obs,
                          int dtype, int64_t N, int64_t ld, void* est, void* resid) {
+  if (M->precision == CS_PRECISION_FP32 && M->gemm) {
+    if (dtype == CS_DTYPE_F32)
+      estimate_gemm<float>(ctx, st, M, static_cast<const float*>(obs), N, ld, static_cast<float*>(est),
+                           static_cast<float*>(resid));
+    else
+      estimate_gemm<double>(ctx, st, M, static_cast<const double*>(obs), N, ld, static_cast<double*>(est),
+                            static_cast<double*>(resid));
+    return;
+  }
   if (M->precision == CS_PRECISION_FP32 && M->tc) {
     if (dtype == CS_DTYPE_F32)
       launch_tc<float>(ctx, st, M, static_cast<const float*>(obs), N, ld, static_cast<float*>(est),
@@ -695,10 +800,12 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
     check_model_shape(M, n);
     if (N == 0) return;
     const bool tc = M->precision == CS_PRECISION_FP32 && M->tc;
-    // chunk: a multiple of the 128-observation tile, ~32 MB of input
-    int64_t Nc = std::max<int64_t>(kObsTile, (int64_t{1} << 22) / std::max<int64_t>(n, 1));
+    const bool gm = M->precision == CS_PRECISION_FP32 && M->gemm;
+    // chunk: a multiple of the 128-observation tile, ~32 MB of input (256 MB
+    // for the two-GEMM path, whose per-launch grid needs more rows)
+    int64_t Nc = std::max<int64_t>(kObsTile, (int64_t{1} << (gm ? 25 : 22)) / std::max<int64_t>(n, 1));
     Nc = (Nc + kObsTile - 1) / kObsTile * kObsTile;
-    if (!tc) Nc = std::max<int64_t>(1, std::min<int64_t>(Nc, (int64_t{1} << 27) / std::max<int64_t>(M->m, 1)));
+    if (!tc && !gm) Nc = std::max<int64_t>(1, std::min<int64_t>(Nc, (int64_t{1} << 27) / std::max<int64_t>(M->m, 1)));
     Nc = std::min(Nc, N);
     cudaEvent_t start;
     CSB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
@@ -720,6 +827,8 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
       double* dr = resid ? ctx->io_res[b].get() : nullptr;
       if (tc) {
         launch_tc<double>(ctx, st, M, ctx->io_in[b].get(), nc, nc, de, dr);
+      } else if (gm) {
+        estimate_gemm<double>(ctx, st, M, ctx->io_in[b].get(), nc, nc, de, dr, b);
       } else {
         estimate_fp64_device(ctx, st, M, ctx->io_in[b].get(), nc, nc, de, dr);
       }
@@ -729,7 +838,7 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
       if (resid)
         CSB_CUDA(cudaMemcpy2DAsync(resid + t0, N * sizeof(double), dr, nc * sizeof(double),
                                    nc * sizeof(double), n, cudaMemcpyDeviceToHost, st));
-      if (!tc) CSB_CUDA(cudaStreamSynchronize(st));  // FP64 path shares one workspace
+      if (!tc && !gm) CSB_CUDA(cudaStreamSynchronize(st));  // FP64 path shares one workspace
     }
     CSB_CUDA(cudaStreamSynchronize(ctx->aux[0]));
     CSB_CUDA(cudaStreamSynchronize(ctx->aux[1]));

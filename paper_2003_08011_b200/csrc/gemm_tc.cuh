@@ -1,0 +1,442 @@
+// gemm_tc.cuh -- large-n MSET2 surveillance as two tcgen05 GEMMs.
+//
+// When the signal count n is too large for the fused kernel's TMEM plan
+// (estimate_tc.cuh keeps an n-wide accumulator plus x and S tiles in TMEM),
+// surveillance runs per observation block as
+//   GEMM-A  ACC[obs, mem] = [x, 1] . [-2 D_norm ; ||d||^2]     (K = n + 1)
+//           epilogue: S = k(ACC + ||x||^2)  -> TF32 hi|lo operand tiles
+//   GEMM-B  O[obs, sig]   = S . P^T,  P = D_norm G+             (K = m)
+//           epilogue: estimate = scale .* O, residual = x - estimate
+// i.e. the reference's sim_matrix -> batched_solve -> matmul chain
+// (mset.cpp:189-193) reassociated as P s, with the similarity
+// map fused into GEMM-A's epilogue and the de-normalisation and residual
+// (mset.cpp:193-197) fused into GEMM-B's.  S exists only as a block-sized
+// FP32-split operand buffer; the reference materialises two m x N FP64
+// matrices (32 GB each at C3).
+//
+// Both GEMMs run the same persistent, warp-specialised kernel:
+//   warp 0     producer: 1D bulk copies (TMA engine) of pre-tiled A and B
+//              operand blocks (hi | lo, canonical K-major, no swizzle) into a
+//              kStages-deep shared-memory ring
+//   warp 1     MMA issuer: per K = 8 slice three tcgen05.mma kind::tf32 (SS)
+//              -- lo.hi + hi.lo + hi.hi (3xTF32, FP32-accurate) -- into one of
+//              two TMEM accumulators (BN columns each)
+//   warps 2-9  epilogue: 2 warps per TMEM lane quarter, each half of the BN
+//              columns, 16 columns per tcgen05.ld; the accumulator is released
+//              as soon as it is read, so the next tile's MMAs overlap.
+#pragma once
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace csb {
+
+constexpr int kGemmBM = 128;      // rows (observations) per tile = TMEM lanes
+constexpr int kGemmBK = 16;       // K per pipeline stage (two k8 slices)
+constexpr int kGemmStages = 4;
+constexpr int kGemmEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kGemmEpiWarps;  // 320
+
+// Operand block of R rows x kGemmBK: hi then lo, canonical K-major layout.
+__host__ __device__ constexpr size_t gemm_block_floats(int R) {
+  return static_cast<size_t>(2) * R * kGemmBK;
+}
+
+// element (r, k) of an R x kGemmBK canonical K-major block, in floats
+__device__ __forceinline__ int canon_idx(int r, int k, int R) {
+  return (r & 7) * 4 + (r >> 3) * 32 + (k & 3) + (k >> 2) * (R / 8) * 32;
+}
+
+struct GemmShape {
+  const float* a;  // [m_tiles][k_chunks] blocks of gemm_block_floats(BM)
+  const float* b;  // [n_tiles][k_chunks] blocks of gemm_block_floats(BN)
+  int m_tiles, n_tiles, k_chunks;
+};
+
+// ------------------------------------------------------------- epilogues
+// GEMM-A: similarity map, written as GEMM-B's A operand (S hi | lo blocks).
+struct EpiSim {
+  float* s_tiles;         // [m_tiles][k_chunks_B] blocks (BM rows)
+  int s_k_chunks;         // = padded m / kGemmBK
+  const float* xx;        // ||x_norm||^2 per observation of the block
+  const float* dd;        // ||d_i||^2 (FP32, padded with 0)
+  const float* dn32;      // n x m D_norm FP32 (direct-difference recompute)
+  const void* obs;        // raw observations of the block (IO type, ld)
+  const float* inv_scale_f;
+  const double* scale_d;
+  int io_f64;
+  int64_t N, ld;
+  int n, m, kind;
+  float inv_h, g_coef, tau, dd_max;
+
+  __device__ float xnorm(int64_t t, int s) const {
+    if (io_f64) return static_cast<float>(static_cast<const double*>(obs)[t + s * ld] / scale_d[s]);
+    return static_cast<const float*>(obs)[t + s * ld] * inv_scale_f[s];
+  }
+  // v: accumulator values of row r (block-relative observation), columns
+  // col0 .. col0 + 15 (memory vectors)
+  __device__ void operator()(int mt, int r, int col0, float* v) const {
+    const int64_t t = static_cast<int64_t>(mt) * kGemmBM + r;
+    const bool valid = t < N;
+    const float xx_r = valid ? xx[t] : 0.f;
+    const float thr = tau * dd_max - (1.f - tau) * xx_r;
+    float mn = v[0];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      mn = fminf(mn, v[e]);
+      v[e] += xx_r;
+    }
+    if (mn < thr && valid) {  // rare: exact near-zero criterion + direct difference
+#pragma unroll 1
+      for (int e = 0; e < 16; ++e) {
+        float cur = 0.f;
+#pragma unroll
+        for (int ee = 0; ee < 16; ++ee)
+          if (ee == e) cur = v[ee];
+        const int col = col0 + e;
+        if (col >= m || !(cur < tau * (xx_r + __ldg(dd + col)))) continue;
+        float a = 0.f;
+        for (int s = 0; s < n; ++s) {
+          const float d = xnorm(t, s) - __ldg(dn32 + static_cast<size_t>(col) * n + s);
+          a = fmaf(d, d, a);
+        }
+#pragma unroll
+        for (int ee = 0; ee < 16; ++ee)
+          if (ee == e) v[ee] = a;
+      }
+    }
+    if (kind == CS_KERNEL_GAUSSIAN) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = ptx::ex2_approx(-fmaxf(v[e], 0.f) * g_coef);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float x = fmaf(ptx::sqrt_approx(fmaxf(v[e], 0.f)), inv_h, 1.f);
+        v[e] = (e & 1) ? ptx::rcp_newton(x) : ptx::rcp_approx(x);
+      }
+    }
+    if (col0 + 16 > m) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (col0 + e >= m) v[e] = 0.f;
+    }
+    // col0 is a multiple of 16 = kGemmBK: the 16 values are one K-chunk row
+    float* blk = s_tiles + (static_cast<size_t>(mt) * s_k_chunks + col0 / kGemmBK) * gemm_block_floats(kGemmBM);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 hi, lo;
+      float* h = &hi.x;
+      float* l = &lo.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float sv = v[4 * q + e];
+        const float hv = __uint_as_float(ptx::to_tf32(sv));
+        h[e] = hv;
+        l[e] = sv - hv;
+      }
+      const int off = canon_idx(r, 4 * q, kGemmBM);
+      *reinterpret_cast<float4*>(blk + off) = hi;
+      *reinterpret_cast<float4*>(blk + kGemmBM * kGemmBK + off) = lo;
+    }
+  }
+};
+
+// GEMM-B: estimate = scale .* O, residual = x - estimate (mset.cpp:193-197).
+template <typename IO>
+struct EpiOut {
+  const IO* obs;  // block-relative, ld
+  IO* est;
+  IO* resid;
+  const float* scale_f;
+  const double* scale_d;
+  int64_t N, ld;
+  int n;
+
+  __device__ void operator()(int mt, int r, int col0, float* v) const {
+    const int64_t t = static_cast<int64_t>(mt) * kGemmBM + r;
+    if (t >= N || col0 >= n) return;
+    IO x[16];
+    if (col0 + 16 <= n) {
+      ptx::ldg8_strided(obs + t + static_cast<int64_t>(col0) * ld, ld, x);
+      ptx::ldg8_strided(obs + t + static_cast<int64_t>(col0 + 8) * ld, ld, x + 8);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = obs[t + static_cast<int64_t>(min(col0 + e, n - 1)) * ld];
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int s = col0 + e;
+      if (s >= n) break;
+      const int64_t idx = t + static_cast<int64_t>(s) * ld;
+      if constexpr (sizeof(IO) == 8) {
+        const double ev = static_cast<double>(v[e]) * scale_d[s];
+        if (est) est[idx] = ev;
+        if (resid) resid[idx] = x[e] - ev;
+      } else {
+        const float ev = v[e] * scale_f[s];
+        if (est) est[idx] = ev;
+        if (resid) resid[idx] = x[e] - ev;
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------------ the kernel
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_tf32_kernel(const GemmShape g, const Epi epi) {
+  static_assert(BN == 128 || BN == 256, "BN");
+  constexpr uint32_t kABytes = gemm_block_floats(kGemmBM) * 4;
+  constexpr uint32_t kBBytes = gemm_block_floats(BN) * 4;
+  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / 32, 0);
+  const int lane = threadIdx.x % 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kGemmStages * kStageBytes);
+  uint64_t* full = bars;                    // [kGemmStages]
+  uint64_t* empty = bars + kGemmStages;     // [kGemmStages]
+  uint64_t* acc_full = bars + 2 * kGemmStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;            // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGemmStages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&acc_full[b], 1);
+      ptx::mbar_init(&acc_empty[b], kGemmEpiWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc(tmem_holder, 2 * BN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  // 2 BN <= 512 columns and one CTA per SM: the allocation starts at column 0
+  if (*tmem_holder != 0u) __trap();
+  constexpr uint32_t tmem = 0;
+
+  const int tiles = g.m_tiles * g.n_tiles;
+  const int KC = g.k_chunks;
+  // tile -> (mt, nt): n fastest, so the CTAs running concurrently share the
+  // A block (observation tile) through L2
+  auto coords = [&](int tile, int& mt, int& nt) {
+    mt = tile / g.n_tiles;
+    nt = tile % g.n_tiles;
+  };
+
+  if (warp == 0) {
+    uint32_t stage = 0, phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int mt, nt;
+      coords(tile, mt, nt);
+      const float* a = g.a + static_cast<size_t>(mt) * KC * gemm_block_floats(kGemmBM);
+      const float* b = g.b + static_cast<size_t>(nt) * KC * gemm_block_floats(BN);
+      for (int kc = 0; kc < KC; ++kc) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* dst = smem + stage * kStageBytes;
+        ptx::mbar_arrive_expect_tx_elect(&full[stage], kStageBytes);
+        ptx::bulk_g2s_elect(dst, a + static_cast<size_t>(kc) * gemm_block_floats(kGemmBM), kABytes, &full[stage]);
+        ptx::bulk_g2s_elect(dst + kABytes, b + static_cast<size_t>(kc) * gemm_block_floats(BN), kBBytes,
+                            &full[stage]);
+        if (++stage == kGemmStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = ptx::idesc_tf32(kGemmBM, BN);
+    constexpr uint32_t LBO_A = (kGemmBM / 8) * 128, LBO_B = (BN / 8) * 128;
+    const uint32_t s0 = ptx::smem_u32(smem);
+    uint32_t stage = 0, phase = 0, local = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      const uint32_t buf = local & 1;
+      ptx::mbar_wait(&acc_empty[buf], ((local >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem + buf * BN;
+      for (int kc = 0; kc < KC; ++kc) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t sa = s0 + stage * kStageBytes, sb = sa + kABytes;
+#pragma unroll
+        for (int k8 = 0; k8 < kGemmBK / 8; ++k8) {
+          const uint64_t ah = ptx::smem_desc(sa + k8 * 2 * LBO_A, LBO_A, 128);
+          const uint64_t al = ptx::smem_desc(sa + kABytes / 2 + k8 * 2 * LBO_A, LBO_A, 128);
+          const uint64_t bh = ptx::smem_desc(sb + k8 * 2 * LBO_B, LBO_B, 128);
+          const uint64_t bl = ptx::smem_desc(sb + kBBytes / 2 + k8 * 2 * LBO_B, LBO_B, 128);
+          ptx::mma_tf32_ss_elect(d, al, bh, idesc, (kc | k8) != 0);
+          ptx::mma_tf32_ss_elect(d, ah, bl, idesc, 1u);
+          ptx::mma_tf32_ss_elect(d, ah, bh, idesc, 1u);
+        }
+        ptx::tc_commit_elect(&empty[stage]);
+        if (++stage == kGemmStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::tc_commit_elect(&acc_full[buf]);
+    }
+  } else {
+    const int ew = warp - 2;            // 0..7
+    const int q = warp & 3;             // TMEM lane quarter
+    const int half = ew >> 2;           // column half
+    const int r = 32 * q + lane;        // tile row
+    const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      int mt, nt;
+      coords(tile, mt, nt);
+      const uint32_t buf = local & 1;
+      ptx::mbar_wait(&acc_full[buf], (local >> 1) & 1);
+      ptx::tc_fence_after();
+      constexpr int kCols = BN / 2;
+      float v[kCols];
+#pragma unroll
+      for (int c = 0; c < kCols / 16; ++c)
+        ptx::tmem_ld16(tmem + lane_off + buf * BN + half * kCols + c * 16, v + c * 16);
+      ptx::tc_wait_ld();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[buf]);  // next tile may accumulate
+#pragma unroll
+      for (int c = 0; c < kCols / 16; ++c) epi(mt, r, nt * BN + half * kCols + c * 16, v + c * 16);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 2 * BN);
+  }
+}
+
+template <int BN>
+constexpr size_t gemm3x_smem_bytes() {
+  return kGemmStages * (gemm_block_floats(kGemmBM) + gemm_block_floats(BN)) * 4 + 256;
+}
+
+// ------------------------------------------------------------- packing
+// Observation block -> GEMM-A operand: x_norm = x / scale augmented with a
+// constant 1 at column n, split hi | lo; ||x_norm||^2 per observation.
+// One thread per (observation, 4 consecutive K).
+template <typename IO>
+__global__ void pack_obs_kernel(const IO* __restrict__ obs, int64_t N, int64_t ld, int n,
+                                const double* __restrict__ scale_d, const float* __restrict__ inv_scale_f,
+                                int k_chunks, float* __restrict__ tiles, float* __restrict__ xx) {
+  const int m_tiles = static_cast<int>((N + kGemmBM - 1) / kGemmBM);
+  const int64_t rows = static_cast<int64_t>(m_tiles) * kGemmBM;
+  const int kq = k_chunks * kGemmBK / 4;
+  const int64_t total = rows * kq;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = e % rows;
+    const int k4 = static_cast<int>(e / rows);
+    float4 hi, lo;
+    float* h = &hi.x;
+    float* l = &lo.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int s = 4 * k4 + i;
+      float v = 0.f;
+      if (t < N) {
+        if (s < n) {
+          if constexpr (sizeof(IO) == 8) {
+            v = static_cast<float>(static_cast<double>(obs[t + s * ld]) / scale_d[s]);
+          } else {
+            v = static_cast<float>(obs[t + s * ld]) * inv_scale_f[s];
+          }
+        } else if (s == n) {
+          v = 1.f;
+        }
+      }
+      const float hv = __uint_as_float(ptx::to_tf32(v));
+      h[i] = hv;
+      l[i] = v - hv;
+    }
+    const int mt = static_cast<int>(t / kGemmBM), r = static_cast<int>(t % kGemmBM);
+    const int kc = (4 * k4) / kGemmBK, kk = (4 * k4) % kGemmBK;
+    float* blk = tiles + (static_cast<size_t>(mt) * k_chunks + kc) * gemm_block_floats(kGemmBM);
+    const int off = canon_idx(r, kk, kGemmBM);
+    *reinterpret_cast<float4*>(blk + off) = hi;
+    *reinterpret_cast<float4*>(blk + kGemmBM * kGemmBK + off) = lo;
+  }
+}
+
+// ||x_norm||^2 per observation (FP32, sequential over signals)
+template <typename IO>
+__global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t ld, int n,
+                                  const double* __restrict__ scale_d, const float* __restrict__ inv_scale_f,
+                                  float* __restrict__ xx) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < N;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float a = 0.f;
+    for (int s = 0; s < n; ++s) {
+      float v;
+      if constexpr (sizeof(IO) == 8) {
+        v = static_cast<float>(static_cast<double>(obs[t + s * ld]) / scale_d[s]);
+      } else {
+        v = static_cast<float>(obs[t + s * ld]) * inv_scale_f[s];
+      }
+      a = fmaf(v, v, a);
+    }
+    xx[t] = a;
+  }
+}
+
+// Model operand for GEMM-A's B side: rows = memory vectors (BN-row tiles),
+// K = signals + the ||d||^2 column; -2 D_norm (exact) and ||d||^2 in FP64.
+__global__ void pack_dn_gemm_kernel(const double* __restrict__ Dn, int n, int m, int BN, int n_tiles,
+                                    int k_chunks, float* __restrict__ out) {
+  const int64_t per = static_cast<int64_t>(BN) * kGemmBK;
+  const int64_t total = per * k_chunks * n_tiles;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t blk = e / per;
+    const int rem = static_cast<int>(e % per);
+    const int nt = static_cast<int>(blk / k_chunks), kc = static_cast<int>(blk % k_chunks);
+    const int r = rem % BN, kk = rem / BN;
+    const int mem = nt * BN + r, k = kc * kGemmBK + kk;
+    double v = 0.0;
+    if (mem < m) {
+      if (k < n) {
+        v = -2.0 * Dn[k + static_cast<int64_t>(mem) * n];
+      } else if (k == n) {
+        for (int s = 0; s < n; ++s) {
+          const double d = Dn[s + static_cast<int64_t>(mem) * n];
+          v = fma(d, d, v);
+        }
+      }
+    }
+    const float hv = __uint_as_float(ptx::to_tf32(static_cast<float>(v)));
+    const float lv = static_cast<float>(v - static_cast<double>(hv));
+    float* o = out + blk * 2 * per;
+    const int off = (r & 7) * 4 + (r >> 3) * 32 + (kk & 3) + (kk >> 2) * (BN / 8) * 32;
+    o[off] = hv;
+    o[per + off] = lv;
+  }
+}
+
+// Model operand for GEMM-B's B side: rows = signals (BN-row tiles), K =
+// memory vectors (padded to k_chunks * kGemmBK); P = D_norm G+ (FP64).
+__global__ void pack_p_gemm_kernel(const double* __restrict__ P, int n, int m, int BN, int n_tiles,
+                                   int k_chunks, float* __restrict__ out) {
+  const int64_t per = static_cast<int64_t>(BN) * kGemmBK;
+  const int64_t total = per * k_chunks * n_tiles;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t blk = e / per;
+    const int rem = static_cast<int>(e % per);
+    const int nt = static_cast<int>(blk / k_chunks), kc = static_cast<int>(blk % k_chunks);
+    const int r = rem % BN, kk = rem / BN;
+    const int sig = nt * BN + r, mem = kc * kGemmBK + kk;
+    const double v = (sig < n && mem < m) ? P[sig + static_cast<int64_t>(mem) * n] : 0.0;
+    const float hv = __uint_as_float(ptx::to_tf32(static_cast<float>(v)));
+    const float lv = static_cast<float>(v - static_cast<double>(hv));
+    float* o = out + blk * 2 * per;
+    const int off = (r & 7) * 4 + (r >> 3) * 32 + (kk & 3) + (kk >> 2) * (BN / 8) * 32;
+    o[off] = hv;
+    o[per + off] = lv;
+  }
+}
+
+}  // namespace csb

@@ -253,7 +253,9 @@ def test_memory_reproduction_fp64(p, oracle):
 @pytest.mark.parametrize("n,m,N,kind", [
     (8, 32, 100, 0), (8, 32, 1000, 1), (20, 100, 1000, 0), (2, 4, 50, 0), (1, 2, 7, 1),
     (64, 512, 3000, 0), (100, 1000, 2000, 0), (100, 1000, 2000, 1), (120, 400, 700, 0),
-    (140, 300, 300, 1), (33, 70, 129, 0)])
+    (140, 300, 300, 1), (33, 70, 129, 0),
+    # large n: two-GEMM path (gemm_tc.cuh)
+    (200, 500, 1000, 0), (257, 600, 700, 1), (131, 262, 129, 0), (512, 1024, 500, 0)])
 def test_fp32_tensor_estimate_within_tolerance(p, oracle, n, m, N, kind):
     X = oracle.synthesize_uniform(n, 4 * m, 0.5, 0.3, 1.0, 0.5, 4.0, 77 + n)
     obs = oracle.synthesize_uniform(n, N, 0.5, 0.3, 1.0, 0.5, 4.0, 91 + n)
@@ -332,6 +334,33 @@ def test_c2_full_size_fp32_properties(p, oracle):
     o = oracle.train(X, 1000, 0, backend=oracle.OPTIMIZED, tile=64, workers=8)
     want = oracle.estimate(o, obs[sel], oracle.OPTIMIZED, 64, 8)[0]
     assert rel(r.estimates[sel], want) <= FP32_TOL
+
+
+def test_large_n_device_resident_and_c3_shape(p, oracle):
+    """Two-GEMM path at BASELINE config 3's model shape (n=1000, m=4000):
+    FP32 device-resident I/O and FP64 host I/O against the FP64 GPU estimate
+    of the same model (bit-exact to the reference order, see
+    test_fp64_estimate_bitwise_given_same_model) on a sample."""
+    import torch
+    import paper_2003_08011_b200 as pk
+    n, m, N = 1000, 4000, 20000
+    X = pk.synthesize(pk.SignalSpec.uniform(n, 4 * m, 0.5, 0.3, 1.0, 0.5, 4.0, 5)).data
+    obs = pk.synthesize(pk.SignalSpec.uniform(n, N, 0.5, 0.3, 1.0, 0.5, 4.0, 6)).data
+    g32 = p.train(X, m, p.KernelConfig(), B(p, "fp32"))
+    g64 = p.train(X, m, p.KernelConfig(), B(p, "fp64"))
+    sel = np.random.default_rng(1).choice(N, 512, replace=False)
+    want = p.estimate(g64, obs[sel]).estimates
+    r = p.estimate(g32, obs)
+    assert np.isfinite(r.estimates).all()
+    assert rel(r.estimates[sel], want) <= FP32_TOL
+    d_obs = torch.tensor(obs.T.copy(), dtype=torch.float32, device="cuda").T
+    d_est = torch.empty_like(d_obs.T).T
+    d_res = torch.empty_like(d_obs.T).T
+    p.estimate_device(g32, d_obs, d_est, d_res)
+    torch.cuda.synchronize()
+    got = d_est.double().cpu().numpy()
+    assert rel(got[sel], want) <= FP32_TOL
+    assert torch.allclose(d_res, d_obs - d_est)
 
 
 def test_cpp_host_layer_on_gpu(p):

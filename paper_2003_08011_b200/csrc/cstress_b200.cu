@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 #include <chrono>
+#include <mutex>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -89,8 +90,14 @@ struct cs_model {
   double h = 0.0;
   int precision = CS_PRECISION_FP64;
   std::vector<int64_t> source_indices;
-  std::vector<double> spectrum_host;
-  DevBuf<double> D, Dn, scale, pinv, spectrum;
+  // eigen_spectrum: computed at train time on the eigen paths; on the
+  // certified-Cholesky path it is materialised on first export (one
+  // eigenvalues-only syevd of the re-formed Gram matrix)
+  mutable std::vector<double> spectrum_host;
+  mutable DevBuf<double> spectrum;
+  mutable bool spectrum_ready = true;
+  mutable std::mutex spectrum_mu;
+  DevBuf<double> D, Dn, scale, pinv;
   // FP32 tensor-core operands (precision == CS_PRECISION_FP32)
   bool tc = false;
   int MT = 0, NB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
@@ -209,7 +216,7 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
 // ---------------------------------------------------------- eigensolver
 // symmetric_eig (mset.cpp:57-70): precondition check, then cuSOLVER syevd
 // (FP64, ascending eigenvalues, orthonormal eigenvectors) in place on V.
-void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
+void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V, bool vectors = true) {
   cudaStream_t st = ctx->stream;
   if (m == 0) return;
   TmpBuf<unsigned long long> stats(2);
@@ -228,18 +235,49 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V) {
   if (!ctx->solver) solver_check(api.create(&ctx->solver), "cusolverDnCreate");
   solver_check(api.set_stream(ctx->solver, st), "SetStream");
   int lwork = 0;
-  solver_check(api.syevd_buffer(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+  const cusolverEigMode_t mode = vectors ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
+  solver_check(api.syevd_buffer(ctx->solver, mode, CUBLAS_FILL_MODE_LOWER,
                                 static_cast<int>(m), V, static_cast<int>(m), w, &lwork),
                "Dsyevd_bufferSize");
   TmpBuf<double> work(static_cast<size_t>(lwork) + 1);
   TmpBuf<int> info(1);
-  solver_check(api.syevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+  solver_check(api.syevd(ctx->solver, mode, CUBLAS_FILL_MODE_LOWER,
                          static_cast<int>(m), V, static_cast<int>(m), w, work.get(), lwork, info.get()),
                "Dsyevd");
   int hinfo = 0;
   CSB_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof hinfo, cudaMemcpyDeviceToHost, st));
   CSB_CUDA(cudaStreamSynchronize(st));
   if (hinfo != 0) fail(CS_EIG_FAILURE, "symmetric_eig: eigensolver did not converge");
+}
+
+// Full-rank fast path of the pseudo-inverse: when every eigenvalue passes the
+// reference cutoff (rank == m), G+ = V L^-1 V^T = G^-1 exactly, computed here
+// by Cholesky factorisation + inverse (~m^3 flops instead of syevd's vector
+// phase and the W W^T product).  Returns false when G is not numerically
+// positive definite, in which case the caller takes the eigenvector path.
+bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
+  cudaStream_t st = ctx->stream;
+  const CusolverApi& api = cusolver_api();
+  if (!ctx->solver) solver_check(api.create(&ctx->solver), "cusolverDnCreate");
+  solver_check(api.set_stream(ctx->solver, st), "SetStream");
+  CSB_CUDA(cudaMemcpyAsync(out, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const int mi = static_cast<int>(m);
+  int l1 = 0, l2 = 0;
+  solver_check(api.potrf_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, &l1), "Dpotrf_bufferSize");
+  solver_check(api.potri_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, &l2), "Dpotri_bufferSize");
+  TmpBuf<double> work(static_cast<size_t>(std::max(l1, l2)) + 1);
+  TmpBuf<int> info(2);
+  solver_check(api.potrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, work.get(), l1, info.get()),
+               "Dpotrf");
+  solver_check(api.potri(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, work.get(), l2, info.get() + 1),
+               "Dpotri");
+  int h[2] = {0, 0};
+  CSB_CUDA(cudaMemcpyAsync(h, info.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  if (h[0] != 0 || h[1] != 0) return false;
+  symmetrize_lower_kernel<<<grid_for(m * m), 256, 0, st>>>(out, m);
+  CSB_LAUNCH_CHECK();
+  return true;
 }
 
 // ------------------------------------------------------ FP32 operand packing
@@ -376,29 +414,85 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->Dn.resize(n * m);                                       // mset.cpp:147-149
   div_rows_kernel<<<grid_for(n * m), 256, 0, st>>>(M->D.get(), M->scale.get(), n, m, M->Dn.get());
   CSB_LAUNCH_CHECK();
-  TmpBuf<double> gram(m * m), V(m * m);                      // mset.cpp:151-152
+  TmpBuf<double> gram(m * m);                                // mset.cpp:151-152
   trace.mark("scale + normalise");
   launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, kind, M->h, gram.get(), m);
   trace.mark("gram (sim_exact)");
-  M->spectrum.resize(m);                                     // mset.cpp:153-154
-  eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get());
-  trace.mark("symmetric_eig (syevd)");
+  // Pseudo-inverse (mset.cpp:153-170).  Fast path: Cholesky inverse of G,
+  // certified full rank -- every eigenvalue of the SPD matrix G satisfies
+  // lambda_min / lambda_max >= 1 / (||G||_1 ||G^-1||_1), so a 1-norm
+  // condition number below kCertifiedCond (half the reference's 1e10
+  // cutoff ratio, margin for rounding) proves rank == m, and then
+  // G+ = V L^-1 V^T = G^-1.  Otherwise the reference's eigen route.
+  const char* force = std::getenv("CSB_TRAIN_EIGVEC");
+  const bool vec_path = force && force[0] == '1';
+  const char* eager_env = std::getenv("CSB_EAGER_SPECTRUM");
+  const bool eager = eager_env && eager_env[0] == '1';
+  M->spectrum.resize(m);
   M->spectrum_host.resize(m);
-  CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
-                           cudaMemcpyDeviceToHost, st));
-  CSB_CUDA(cudaStreamSynchronize(st));
-  const double cutoff = 1e-10 * M->spectrum_host[m - 1];    // mset.cpp:156-163
-  int64_t rank = 0;
-  for (int64_t i = 0; i < m; ++i)
-    if (M->spectrum_host[i] > cutoff) ++rank;
-  if (rank == 0) fail(CS_DEGENERATE_MODEL, "train: all Gram eigenvalues below cutoff");
-  M->rank = rank;
-  TmpBuf<double> W(m * rank);                                // mset.cpp:165-170
-  whiten_kernel<<<grid_for(m * rank), 256, 0, st>>>(V.get(), M->spectrum.get(), m, rank, W.get());
-  CSB_LAUNCH_CHECK();
   M->pinv.resize(m * m);
-  launch_gemm_exact<false, true>(st, W.get(), m, W.get(), m, m, rank, m, M->pinv.get(), m);
-  trace.mark("pinv (W W^T)");
+  bool done = false;
+  int64_t rank = 0;
+  if (!vec_path && !eager && cholesky_inverse(ctx, gram.get(), m, M->pinv.get())) {
+    TmpBuf<unsigned long long> nrm(2);
+    CSB_CUDA(cudaMemsetAsync(nrm.get(), 0, 2 * sizeof(unsigned long long), st));
+    const int nb = static_cast<int>(std::min<int64_t>(m, 4 * 148));
+    norm1_kernel<<<nb, 256, 0, st>>>(gram.get(), m, nrm.get());
+    norm1_kernel<<<nb, 256, 0, st>>>(M->pinv.get(), m, nrm.get() + 1);
+    CSB_LAUNCH_CHECK();
+    unsigned long long hb[2];
+    CSB_CUDA(cudaMemcpyAsync(hb, nrm.get(), sizeof hb, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    double g1, gi1;
+    std::memcpy(&g1, &hb[0], 8);
+    std::memcpy(&gi1, &hb[1], 8);
+    constexpr double kCertifiedCond = 5e9;
+    if (std::isfinite(g1 * gi1) && g1 * gi1 < kCertifiedCond) {
+      rank = m;
+      done = true;
+      M->spectrum_ready = false;
+    }
+    trace.mark("pinv (certified Cholesky)");
+  }
+  TmpBuf<double> V;  // syevd works in place on a copy of G
+  if (!done) {
+    // eigenvalues first: they decide the rank exactly as the reference does
+    V.resize(m * m);
+    eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), vec_path);
+    trace.mark(vec_path ? "symmetric_eig (syevd)" : "eigenvalues (syevd N)");
+    CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    const double cutoff = 1e-10 * M->spectrum_host[m - 1];  // mset.cpp:156-163
+    for (int64_t i = 0; i < m; ++i)
+      if (M->spectrum_host[i] > cutoff) ++rank;
+    if (rank == 0) fail(CS_DEGENERATE_MODEL, "train: all Gram eigenvalues below cutoff");
+    if (rank == m && !vec_path) {
+      done = cholesky_inverse(ctx, gram.get(), m, M->pinv.get());
+      trace.mark("pinv (Cholesky inverse)");
+    }
+  }
+  M->rank = rank;
+  if (!done) {
+    if (!vec_path) {
+      eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), true);
+      trace.mark("symmetric_eig (syevd V)");
+      CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+      CSB_CUDA(cudaStreamSynchronize(st));
+      const double c2 = 1e-10 * M->spectrum_host[m - 1];
+      rank = 0;
+      for (int64_t i = 0; i < m; ++i)
+        if (M->spectrum_host[i] > c2) ++rank;
+      if (rank == 0) fail(CS_DEGENERATE_MODEL, "train: all Gram eigenvalues below cutoff");
+      M->rank = rank;
+    }
+    TmpBuf<double> W(m * rank);                              // mset.cpp:165-170
+    whiten_kernel<<<grid_for(m * rank), 256, 0, st>>>(V.get(), M->spectrum.get(), m, rank, W.get());
+    CSB_LAUNCH_CHECK();
+    launch_gemm_exact<false, true>(st, W.get(), m, W.get(), m, m, rank, m, M->pinv.get(), m);
+    trace.mark("pinv (W W^T)");
+  }
   if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
   CSB_CUDA(cudaStreamSynchronize(st));
   trace.mark("fp32 operand packing");
@@ -602,6 +696,27 @@ void estimate_device_any(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const 
 }
 
 }  // namespace
+
+// eigen_spectrum of a model trained on the certified-Cholesky path: re-form
+// the Gram matrix (bitwise the one train factorised) and take its
+// eigenvalues on a private context.
+void materialize_spectrum(const cs_model* M) {
+  std::lock_guard<std::mutex> lock(M->spectrum_mu);
+  if (M->spectrum_ready) return;
+  cs_ctx* ctx = nullptr;
+  if (cs_ctx_create(M->device, &ctx) != CS_OK) fail(CS_ERROR, "eigen_spectrum: " + g_last_error);
+  std::unique_ptr<cs_ctx, cs_status (*)(cs_ctx*)> guard(ctx, cs_ctx_destroy);
+  StreamScope scope(ctx->stream);
+  const int64_t n = M->n, m = M->m;
+  TmpBuf<double> gram(m * m), V(m * m);
+  launch_sim_exact(ctx->stream, M->Dn.get(), n, M->Dn.get(), n, n, m, m, M->kind, M->h, gram.get(), m);
+  M->spectrum.resize(m);
+  eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), false);
+  CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  CSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  M->spectrum_ready = true;
+}
 
 // ======================================================================= ABI
 extern "C" {
@@ -868,7 +983,10 @@ cs_status cs_model_export(const cs_model* M, int64_t* idx, double* D, double* pi
     if (idx) std::memcpy(idx, M->source_indices.data(), m * sizeof(int64_t));
     if (D) CSB_CUDA(cudaMemcpy(D, M->D.get(), n * m * sizeof(double), cudaMemcpyDeviceToHost));
     if (pinv) CSB_CUDA(cudaMemcpy(pinv, M->pinv.get(), m * m * sizeof(double), cudaMemcpyDeviceToHost));
-    if (spectrum) std::memcpy(spectrum, M->spectrum_host.data(), m * sizeof(double));
+    if (spectrum) {
+      materialize_spectrum(M);
+      std::memcpy(spectrum, M->spectrum_host.data(), m * sizeof(double));
+    }
     if (scale) CSB_CUDA(cudaMemcpy(scale, M->scale.get(), n * sizeof(double), cudaMemcpyDeviceToHost));
   });
 }

@@ -289,4 +289,35 @@ __global__ void whiten_kernel(const double* __restrict__ V, const double* __rest
   }
 }
 
+// Mirror the lower triangle into the upper one (potri writes the lower
+// triangle of the inverse only).
+__global__ void symmetrize_lower_kernel(double* __restrict__ A, int64_t m) {
+  const int64_t total = m * m;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % m, j = e / m;  // column-major (i, j)
+    if (i < j) A[e] = A[j + i * m];
+  }
+}
+
+// ||A||_1 = max_j sum_i |A_ij| of a column-major m x m matrix; one block per
+// column, maximum folded into *out as the bit pattern of a non-negative
+// double (ordered like the value).
+__global__ void norm1_kernel(const double* __restrict__ A, int64_t m, unsigned long long* out) {
+  __shared__ double part[32];
+  for (int64_t j = blockIdx.x; j < m; j += gridDim.x) {
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) a += fabs(A[i + j * m]);
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      a = threadIdx.x < blockDim.x / 32 ? part[threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (threadIdx.x == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(a)));
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace csb

@@ -29,6 +29,13 @@ struct CusolverApi {
                                    const double*, int, const double*, int*) = nullptr;
   cusolverStatus_t (*syevd)(cusolverDnHandle_t, cusolverEigMode_t, cublasFillMode_t, int, double*,
                             int, double*, double*, int, int*) = nullptr;
+  // Cholesky factor / inverse (full-rank fast path of the pseudo-inverse)
+  cusolverStatus_t (*potrf_buffer)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, int*) = nullptr;
+  cusolverStatus_t (*potrf)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, double*, int,
+                            int*) = nullptr;
+  cusolverStatus_t (*potri_buffer)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, int*) = nullptr;
+  cusolverStatus_t (*potri)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, double*, int,
+                            int*) = nullptr;
 };
 
 inline const CusolverApi& cusolver_api() {
@@ -61,7 +68,14 @@ inline const CusolverApi& cusolver_api() {
     api.syevd_buffer =
         reinterpret_cast<decltype(api.syevd_buffer)>(dlsym(api.lib, "cusolverDnDsyevd_bufferSize"));
     api.syevd = reinterpret_cast<decltype(api.syevd)>(dlsym(api.lib, "cusolverDnDsyevd"));
-    if (!api.create || !api.destroy || !api.set_stream || !api.syevd_buffer || !api.syevd) {
+    api.potrf_buffer =
+        reinterpret_cast<decltype(api.potrf_buffer)>(dlsym(api.lib, "cusolverDnDpotrf_bufferSize"));
+    api.potrf = reinterpret_cast<decltype(api.potrf)>(dlsym(api.lib, "cusolverDnDpotrf"));
+    api.potri_buffer =
+        reinterpret_cast<decltype(api.potri_buffer)>(dlsym(api.lib, "cusolverDnDpotri_bufferSize"));
+    api.potri = reinterpret_cast<decltype(api.potri)>(dlsym(api.lib, "cusolverDnDpotri"));
+    if (!api.create || !api.destroy || !api.set_stream || !api.syevd_buffer || !api.syevd ||
+        !api.potrf_buffer || !api.potrf || !api.potri_buffer || !api.potri) {
       error += "missing cuSOLVER symbols in " + api.path;
       api.lib = nullptr;
     }

@@ -248,6 +248,56 @@ def run_bench_sweep(world, rank, local, barrier, max_over_ranks):
 
 
 # ---------------------------------------------------------------------- B200
+def run_c3(args, local):
+    """BASELINE configs[2] (C3: n=1000, N=1M, m=4000, 16k training rows) on
+    one GPU: train time through the host API and device-resident FP32
+    surveillance on the two-GEMM tcgen05 path.  Data from the device
+    synthesiser (same recipe; host synthesis of 1e9 samples is impractical)."""
+    import torch
+    import paper_2003_08011_b200 as p
+    n, N, m = 1000, 1_000_000, 4000
+    dev = torch.device("cuda", local)
+    t = TEMPLATE
+    base = p.cell_data_seed(MASTER_SEED, n, N, m, 0)
+    spec = lambda rows, seed: p.SignalSpec.uniform(n, rows, t["phi"], t["rho"], t["var"], t["skew"],  # noqa: E731
+                                                   t["kurt"], seed)
+    X = p.synthesize_device(spec(TRAIN_FACTOR * m, p.derive_seed(base, [0])), local)
+    backend = p.BackendId("b200", local, "fp32")
+    p.train_device(X, m, p.KernelConfig(), backend)  # warm (cuSOLVER kernels for this size)
+    tt = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        model = p.train_device(X, m, p.KernelConfig(), backend)
+        tt.append(time.perf_counter() - t0)
+    del X
+    obs64 = p.synthesize_device(spec(N, p.derive_seed(base, [1])), local)
+    obs = obs64.T.float().T          # N x n column-major FP32
+    del obs64
+    est = torch.empty_like(obs.T).T
+    res = torch.empty_like(obs.T).T
+    st = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        p.estimate_device(model, obs, est, res, st)
+    steps = 5
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        a.record(st)
+        p.estimate_device(model, obs, est, res, st)
+        b.record(st)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    flops = 4.0 * n * m * N
+    tf32 = load_tf32_peak() or 1190.0
+    return {"workload": "C3: n=1000, N=1,000,000, m=4,000 (16k training rows), FP32 device-resident I/O",
+            "obs_per_s": N / (ms * 1e-3), "ms_per_pass": ms, "steps": steps,
+            "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
+            "frac_3xtf32": flops / (ms * 1e-3) / 1e12 / (tf32 / 3),
+            "kernels": "pack_obs + gemm3x_tf32_kernel<256,EpiSim> + gemm3x_tf32_kernel<256,EpiOut> per 32,768-observation block",
+            "train_ms": statistics.median(tt) * 1e3,
+            "train_api": "cs_mset_train_device (device FP64 training rows, synchronous)"}
+
+
 def run_b200(args, world, rank, local):
     import numpy as np
     import torch
@@ -282,6 +332,16 @@ def run_b200(args, world, rank, local):
         model = p.train(train, N_MEM, p.KernelConfig(), backend)
         train_times.append(time.perf_counter() - t0)
     train_ms = statistics.median(train_times) * 1e3
+    # same call with the eigen_spectrum computed inside train (eigenvalues-only
+    # syevd; the default path defers it to the first export)
+    os.environ["CSB_EAGER_SPECTRUM"] = "1"
+    eager = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        p.train(train, N_MEM, p.KernelConfig(), backend)
+        eager.append(time.perf_counter() - t0)
+    del os.environ["CSB_EAGER_SPECTRUM"]
+    train_eager_ms = statistics.median(eager) * 1e3
 
     # ---- device-resident surveillance
     d_obs = torch.tensor(obs.T.astype(np.float32), device=dev).T          # N x n col-major
@@ -351,7 +411,7 @@ def run_b200(args, world, rank, local):
     achieved_tflops = flops_per_obs * N_OBS / (mean_ms * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops", 1590.0)
     # tensor work actually issued: 3 TF32 products per GEMM incl. padding
-    K1, N2 = (N_SIG + 7) // 8 * 8, (N_SIG + 15) // 16 * 16
+    K1, N2 = (N_SIG + 1 + 7) // 8 * 8, (N_SIG + 15) // 16 * 16
     MT = 64  # tile the library selects for n = 100 (choose_tc_shape)
     tf32_peak = load_tf32_peak() or bf16 / 2
     m_pad = (N_MEM + MT - 1) // MT * MT
@@ -374,7 +434,10 @@ def run_b200(args, world, rank, local):
         "wall_s_timed_region": wall,
         "gpu_launches": args.steps,
         "train": {"ms": train_ms, "api": "cs_mset_train (host FP64 in, synchronous)",
-                  "includes": "selection + scale + Gram + cuSOLVER syevd + pseudo-inverse + P=Dn G+ + operand packing"},
+                  "includes": "H2D + selection + scale + Gram + certified-Cholesky pseudo-inverse (rank == m "
+                              "proven by the 1-norm condition bound; eigen route otherwise) + P=Dn G+ + "
+                              "operand packing; eigen_spectrum deferred to first export",
+                  "ms_with_eigen_spectrum": train_eager_ms},
         "e2e": {"value": world * N_OBS / e2e_mean, "unit": UNIT,
                 "h2d_bytes_per_step": N_OBS * N_SIG * 8,
                 "d2h_bytes_per_step": 2 * N_OBS * N_SIG * 8,
@@ -396,6 +459,8 @@ def run_b200(args, world, rank, local):
     }
     if sweep is not None:
         line["sweep"] = sweep
+    if world == 1 and not args.no_c3:
+        line["c3"] = run_c3(args, local)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(train, obs)
     print(json.dumps(line), flush=True)
@@ -409,6 +474,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

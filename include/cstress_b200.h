@@ -153,6 +153,37 @@ cs_status cs_model_import(cs_ctx* ctx, int64_t n, int64_t m, int kernel_kind,
                           cs_model** out);
 cs_status cs_model_destroy(cs_model* model);
 
+/* CSM1 model files (save_model / load_model, mset.cpp:225-310; declared at
+ * mset.hpp:83-86): byte-compatible with the reference writer, including the
+ * "<path>.json" sidecar.  Errors: CS_IO_ERROR with the reference texts
+ * ("load_model: bad magic in <path>", "... truncated file ...", ...). */
+cs_status cs_model_save(const cs_model* model, const char* path);
+cs_status cs_model_load(cs_ctx* ctx, const char* path, int precision,
+                        cs_model** out);
+
+/* ------------------------------------------------------------------ SPRT
+ * Wald sequential probability ratio test on residual streams (north_star
+ * "SPRT alarm flags").  NOT in the reference, so the
+ * definition is this project's, checked bit-for-bit against
+ * oracle/cstress_oracle.c:or_sprt (parity against the reference: unpinned).
+ * Per signal s: positive test lambda += c[s]*(r - h[s]), negative test
+ * lambda += c[s]*((-r) - h[s]) (FP64, that operation order, no FMA);
+ * lambda >= B -> alarm (flags bit 0 / bit 1) and lambda = 0; lambda <= A ->
+ * lambda = 0.  Typical: M = k sigma, c = M / sigma^2, h = M / 2,
+ * A = ln(beta / (1 - alpha)), B = ln((1 - beta) / alpha).
+ * state: 2 doubles per signal (positive, negative), carried across calls.
+ * flags: N x n column-major uint8; counts: 2 per signal (may be NULL). */
+cs_status cs_sprt(cs_ctx* ctx, const double* residuals /* N x n host */,
+                  int64_t N, int64_t n, const double* c, const double* h,
+                  double A, double B, double* state, uint8_t* flags,
+                  int64_t* counts);
+/* residuals on the device (FP64 or FP32, leading dimension ld); flags on
+ * the device (leading dimension N); c, h, state, counts on the host. */
+cs_status cs_sprt_device(cs_ctx* ctx, const void* d_residuals, int dtype,
+                         int64_t N, int64_t n, int64_t ld, const double* c,
+                         const double* h, double A, double B, double* state,
+                         uint8_t* d_flags, int64_t* counts);
+
 /* ------------------------------------------------------------ data feed
  * synthesize (signals.cpp:205-254) for SignalSpec::uniform (signals.cpp:51-65),
  * host FP64 output N x n.  Seeds per rng.hpp:26-33. */

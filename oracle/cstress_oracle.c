@@ -1182,3 +1182,37 @@ uint64_t or_cell_data_seed(uint64_t master_seed, int64_t n_signals,
                          (uint64_t)n_memory, (uint64_t)replicate};
   return or_derive_seed(master_seed, c, 4);
 }
+
+/* ------------------------------------------------------------------ SPRT
+ * Wald sequential probability ratio test on residual streams -- NOT in the
+ * reference (SPEC.md:14, :190 exclude anomaly decision logic), so this is
+ * the project's own definition, the checker for the GPU's alarm flags
+ * (parity unpinned against the reference).  Per signal s, two one-sided
+ * mean tests against H0: r ~ N(0, sigma_s^2):
+ *   positive  lambda += c_s * (r - h_s)          (H1: mean +M_s)
+ *   negative  lambda += c_s * ((-r) - h_s)       (H2: mean -M_s)
+ * with c_s = M_s / sigma_s^2 and h_s = M_s / 2 supplied by the caller, in
+ * that operation order (no FMA).  lambda >= B: alarm, flag bit set,
+ * lambda = 0; else lambda <= A: accept H0, lambda = 0.  Flags: bit 0
+ * positive alarm, bit 1 negative alarm.  state (2 per signal: positive,
+ * negative) carries lambda across calls. */
+void or_sprt(const double* resid, int64_t N, int64_t n, int64_t ld, const double* c,
+             const double* h, double A, double B, double* state, uint8_t* flags,
+             int64_t* counts) {
+  for (int64_t s = 0; s < n; ++s) {
+    double lp = state[2 * s], ln = state[2 * s + 1];
+    int64_t cp = 0, cn = 0;
+    for (int64_t t = 0; t < N; ++t) {
+      const double r = resid[t + s * ld];
+      uint8_t f = 0;
+      lp = lp + c[s] * (r - h[s]);
+      if (lp >= B) { f |= 1; lp = 0.0; ++cp; } else if (lp <= A) { lp = 0.0; }
+      ln = ln + c[s] * ((-r) - h[s]);
+      if (ln >= B) { f |= 2; ln = 0.0; ++cn; } else if (ln <= A) { ln = 0.0; }
+      flags[t + s * N] = f;
+    }
+    state[2 * s] = lp;
+    state[2 * s + 1] = ln;
+    if (counts) { counts[2 * s] = cp; counts[2 * s + 1] = cn; }
+  }
+}

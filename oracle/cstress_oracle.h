@@ -124,4 +124,9 @@ uint64_t or_cell_data_seed(uint64_t master_seed, int64_t n_signals,
 #ifdef __cplusplus
 }
 #endif
+/* SPRT on residual streams (project definition; no reference counterpart). */
+void or_sprt(const double* resid, int64_t N, int64_t n, int64_t ld, const double* c,
+             const double* h, double A, double B, double* state, uint8_t* flags,
+             int64_t* counts);
+
 #endif

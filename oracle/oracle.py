@@ -82,6 +82,8 @@ def lib():
             "or_estimate": (i32, [pd, pd, pd, i64, i64, i64, i32, d, pd, i64, i32,
                                   i32, i32, pd, pd]),
             "or_cell_data_seed": (u64, [u64, i64, i64, i64, i32]),
+            "or_sprt": (None, [pd, i64, i64, i64, pd, pd, C.c_double, C.c_double, pd,
+                               C.POINTER(C.c_uint8), pi64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -303,3 +305,93 @@ def generate_cells(signal_counts, observation_counts, memory_counts):
             for obs in observation_counts:
                 cells.append(((n, obs, m), m >= 2 * n))
     return cells
+
+
+# ------------------------------------------------------------ model files
+def _json_double(v: float) -> str:
+    """nlohmann::json number formatting: shortest round-trip, '.0' kept."""
+    s = repr(float(v))
+    return s
+
+
+def save_model_csm1(model, path: str) -> None:
+    """save_model (mset.cpp:229-267): "CSM1", u32 1, u64 n, u64 m,
+    u32 kind (1 = gaussian), f64 bandwidth, u64 rank, D, gram_pinv,
+    eigen_spectrum, signal_scale (column-major FP64), m x u64 source indices;
+    plus the nlohmann dump(2) sidecar "<path>.json" (keys sorted)."""
+    import struct
+    D = _f64(model.D)
+    n, m = D.shape
+    with open(path, "wb") as f:
+        f.write(b"CSM1")
+        f.write(struct.pack("<IQQIdQ", 1, n, m, 1 if model.kind == GAUSSIAN else 0, model.h, model.rank))
+        f.write(np.asarray(D, dtype="<f8").tobytes(order="F"))
+        f.write(np.asarray(_f64(model.gram_pinv), dtype="<f8").tobytes(order="F"))
+        f.write(np.asarray(model.eigen_spectrum, dtype="<f8").tobytes())
+        f.write(np.asarray(model.scale, dtype="<f8").tobytes())
+        f.write(np.asarray(model.source_indices, dtype="<u8").tobytes())
+    kind = "gaussian" if model.kind == GAUSSIAN else "inverse_distance"
+    with open(path + ".json", "w") as f:
+        f.write("{\n  \"format\": \"CSM1\",\n  \"kernel\": {\n"
+                f"    \"bandwidth\": {_json_double(model.h)},\n    \"kind\": \"{kind}\"\n  }},\n"
+                f"  \"n_memory\": {m},\n  \"n_signals\": {n},\n  \"rank\": {model.rank},\n"
+                "  \"version\": 1\n}\n")
+
+
+def load_model_csm1(path: str):
+    """load_model (mset.cpp:269-310); raises OracleError(8, ...) with the
+    reference texts."""
+    import struct
+    try:
+        data = open(path, "rb").read()
+    except OSError:
+        raise OracleError(8, f"load_model: cannot open {path}")
+    if data[:4] != b"CSM1":
+        raise OracleError(8, f"load_model: bad magic in {path}")
+    if len(data) < 8 or struct.unpack_from("<I", data, 4)[0] != 1:
+        raise OracleError(8, f"load_model: unsupported version in {path}")
+    hdr = struct.calcsize("<IQQIdQ")
+    if len(data) < 4 + hdr:
+        raise OracleError(8, f"load_model: truncated file {path}")
+    _, n, m, kind, h, rank = struct.unpack_from("<IQQIdQ", data, 4)
+    off = 4 + hdr
+    need = 8 * (n * m + m * m + m + n + m)
+    if len(data) < off + need:
+        raise OracleError(8, f"load_model: truncated file {path}")
+    def take(count, dt="<f8"):
+        nonlocal off
+        a = np.frombuffer(data, dtype=dt, count=count, offset=off)
+        off += 8 * count
+        return a
+    D = take(n * m).reshape((n, m), order="F").copy(order="F")
+    pinv = take(m * m).reshape((m, m), order="F").copy(order="F")
+    spec = take(m).copy()
+    scale = take(n).copy()
+    idx = take(m, "<u8").astype(np.int64)
+    return Model(source_indices=idx, D=D, scale=scale, gram_pinv=pinv, eigen_spectrum=spec,
+                 rank=int(rank), h=float(h), kind=GAUSSIAN if kind == 1 else INVERSE_DISTANCE)
+
+
+# ------------------------------------------------------------------ SPRT
+def sprt_params(sigma, k=3.0, alpha=1e-3, beta=1e-3):
+    """Per-signal c = M / sigma^2, h = M / 2 with M = k sigma; Wald
+    thresholds A = ln(beta / (1 - alpha)), B = ln((1 - beta) / alpha)."""
+    import math
+    sigma = np.asarray(sigma, dtype=np.float64)
+    M = k * sigma
+    c = M / (sigma * sigma)
+    h = M / 2.0
+    return c, h, math.log(beta / (1.0 - alpha)), math.log((1.0 - beta) / alpha)
+
+
+def sprt(resid, c, h, A, B, state=None):
+    """or_sprt: returns (flags N x n uint8 column-major, state (n, 2), counts (n, 2))."""
+    r = _f64(resid)
+    N, n = r.shape
+    st = np.zeros((n, 2)) if state is None else np.array(state, dtype=np.float64).reshape(n, 2).copy()
+    flags = np.zeros((N, n), dtype=np.uint8, order="F")
+    counts = np.zeros((n, 2), dtype=np.int64)
+    lib().or_sprt(_pd(r), N, n, max(N, 1), _pd(np.ascontiguousarray(c, dtype=np.float64)),
+                  _pd(np.ascontiguousarray(h, dtype=np.float64)), A, B, _pd(st),
+                  flags.ctypes.data_as(C.POINTER(C.c_uint8)), _pi64(counts))
+    return flags, st, counts

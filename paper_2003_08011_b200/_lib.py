@@ -47,6 +47,10 @@ _SIGNATURES = {
     "cs_model_export": (i32, [vp, pi64, pd, pd, pd, pd]),
     "cs_model_import": (i32, [vp, i64, i64, i32, d, i64, pi64, pd, pd, pd, pd, i32, P(vp)]),
     "cs_model_destroy": (i32, [vp]),
+    "cs_model_save": (i32, [vp, C.c_char_p]),
+    "cs_sprt": (i32, [vp, pd, i64, i64, pd, pd, d, d, pd, P(C.c_uint8), pi64]),
+    "cs_sprt_device": (i32, [vp, vp, i32, i64, i64, i64, pd, pd, d, d, pd, vp, pi64]),
+    "cs_model_load": (i32, [vp, C.c_char_p, i32, P(vp)]),
     "cs_synthesize_uniform": (i32, [i64, i64, d, d, d, d, d, u64, pd]),
     "cs_synthesize_uniform_device": (i32, [vp, i64, i64, d, d, d, d, d, u64, vp]),
     "cs_derive_seed": (u64, [u64, pu64, i32]),

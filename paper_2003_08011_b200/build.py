@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcstress_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["cstress_b200.cu", "synth.cpp", "host.cpp"]
+SOURCES = ["cstress_b200.cu", "synth.cpp", "model_io.cpp"]
 
 
 def _sources():

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "estimate_tc.cuh"
 #include "gemm_tc.cuh"
+#include "sprt.cuh"
 #include "kernels_f64.cuh"
 #include "selection.cuh"
 #include "solver.cuh"
@@ -697,6 +698,38 @@ void estimate_device_any(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const 
 
 }  // namespace
 
+// SPRT over device residuals (sprt.cuh); state / counts are host arrays.
+template <typename IO>
+void sprt_device(cs_ctx* ctx, const IO* resid, int64_t N, int64_t n, int64_t ld, const double* c,
+                 const double* h, double A, double B, double* state, uint8_t* d_flags, int64_t* counts) {
+  cudaStream_t st = ctx->stream;
+  for (int64_t s = 0; s < n; ++s)
+    if (!(c[s] > 0.0) || !std::isfinite(c[s]) || !std::isfinite(h[s]))
+      fail(CS_CONFIG_ERROR, "sprt: per-signal coefficients must be finite and c > 0");
+  if (!(A < 0.0 && B > 0.0)) fail(CS_CONFIG_ERROR, "sprt: thresholds must satisfy A < 0 < B");
+  if (N == 0 || n == 0) return;
+  const int chunks = static_cast<int>((N + kSprtChunk - 1) / kSprtChunk);
+  TmpBuf<double> dc(n), dh(n), dstate(2 * n), spec(static_cast<size_t>(2) * n * chunks);
+  TmpBuf<unsigned long long> dcount(2 * n);
+  CSB_CUDA(cudaMemcpyAsync(dc.get(), c, n * 8, cudaMemcpyHostToDevice, st));
+  CSB_CUDA(cudaMemcpyAsync(dh.get(), h, n * 8, cudaMemcpyHostToDevice, st));
+  CSB_CUDA(cudaMemcpyAsync(dstate.get(), state, 2 * n * 8, cudaMemcpyHostToDevice, st));
+  sprt_speculate_kernel<IO><<<grid_for(n * chunks, 128), 128, 0, st>>>(
+      resid, N, static_cast<int>(n), ld, dc.get(), dh.get(), A, B, dstate.get(), chunks, d_flags, spec.get());
+  CSB_LAUNCH_CHECK();
+  sprt_fixup_kernel<IO><<<ceil_div(n, 64), 64, 0, st>>>(resid, N, static_cast<int>(n), ld, dc.get(), dh.get(), A,
+                                                        B, dstate.get(), chunks, d_flags, spec.get());
+  CSB_LAUNCH_CHECK();
+  sprt_count_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_flags, N, static_cast<int>(n), dcount.get());
+  CSB_LAUNCH_CHECK();
+  std::vector<unsigned long long> hc(2 * n);
+  CSB_CUDA(cudaMemcpyAsync(state, dstate.get(), 2 * n * 8, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaMemcpyAsync(hc.data(), dcount.get(), 2 * n * 8, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  if (counts)
+    for (int64_t i = 0; i < 2 * n; ++i) counts[i] = static_cast<int64_t>(hc[i]);
+}
+
 // eigen_spectrum of a model trained on the certified-Cholesky path: re-form
 // the Gram matrix (bitwise the one train factorised) and take its
 // eigenvalues on a private context.
@@ -958,6 +991,41 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
     CSB_CUDA(cudaStreamSynchronize(ctx->aux[0]));
     CSB_CUDA(cudaStreamSynchronize(ctx->aux[1]));
     cudaEventDestroy(start);
+  });
+}
+
+cs_status cs_sprt_device(cs_ctx* ctx, const void* d_resid, int dtype, int64_t N, int64_t n, int64_t ld,
+                         const double* c, const double* h, double A, double B, double* state,
+                         uint8_t* d_flags, int64_t* counts) {
+  return guarded([&] {
+    if (!ctx || !c || !h || !state || (!d_flags && N * n > 0)) fail(CS_CONFIG_ERROR, "sprt: null argument");
+    if (ld < N) fail(CS_SHAPE_ERROR, "sprt: leading dimension smaller than observation count");
+    set_device(ctx->device);
+    StreamScope scope(ctx->stream);
+    if (dtype == CS_DTYPE_F64)
+      sprt_device<double>(ctx, static_cast<const double*>(d_resid), N, n, ld, c, h, A, B, state, d_flags, counts);
+    else if (dtype == CS_DTYPE_F32)
+      sprt_device<float>(ctx, static_cast<const float*>(d_resid), N, n, ld, c, h, A, B, state, d_flags, counts);
+    else
+      fail(CS_CONFIG_ERROR, "sprt: unknown dtype");
+  });
+}
+
+cs_status cs_sprt(cs_ctx* ctx, const double* resid, int64_t N, int64_t n, const double* c, const double* h,
+                  double A, double B, double* state, uint8_t* flags, int64_t* counts) {
+  return guarded([&] {
+    if (!ctx || !c || !h || !state || (!resid && N * n > 0)) fail(CS_CONFIG_ERROR, "sprt: null argument");
+    set_device(ctx->device);
+    StreamScope scope(ctx->stream);
+    TmpBuf<double> dr(static_cast<size_t>(N) * n + 1);
+    TmpBuf<uint8_t> df(static_cast<size_t>(N) * n + 1);
+    if (N * n > 0)
+      CSB_CUDA(cudaMemcpyAsync(dr.get(), resid, N * n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    sprt_device<double>(ctx, dr.get(), N, n, N, c, h, A, B, state, df.get(), counts);
+    if (flags && N * n > 0) {
+      CSB_CUDA(cudaMemcpyAsync(flags, df.get(), N * n, cudaMemcpyDeviceToHost, ctx->stream));
+      CSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
   });
 }
 

@@ -369,8 +369,25 @@ __global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t
                                   float* __restrict__ xx) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < N;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // sequential sum over signals (deterministic); eight independent loads
+    // in flight per step
     float a = 0.f;
-    for (int s = 0; s < n; ++s) {
+    int s = 0;
+    for (; s + 8 <= n; s += 8) {
+      IO r[8];
+      ptx::ldg8_strided(obs + t + static_cast<int64_t>(s) * ld, ld, r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float v;
+        if constexpr (sizeof(IO) == 8) {
+          v = static_cast<float>(static_cast<double>(r[e]) / scale_d[s + e]);
+        } else {
+          v = static_cast<float>(r[e]) * inv_scale_f[s + e];
+        }
+        a = fmaf(v, v, a);
+      }
+    }
+    for (; s < n; ++s) {
       float v;
       if constexpr (sizeof(IO) == 8) {
         v = static_cast<float>(static_cast<double>(obs[t + s * ld]) / scale_d[s]);

@@ -348,6 +348,19 @@ def import_model(D, signal_scale, gram_pinv, rank, cfg: KernelConfig,
     return TrainedModel(h, backend)
 
 
+def save_model(model: TrainedModel, path: str) -> None:
+    """save_model (mset.hpp:85, mset.cpp:229-267): CSM1 binary + .json sidecar."""
+    check(_lib.lib().cs_model_save(model.handle, str(path).encode()))
+
+
+def load_model(path: str, backend: BackendId = BackendId()) -> TrainedModel:
+    """load_model (mset.hpp:86, mset.cpp:269-310) onto the backend's device."""
+    h = C.c_void_p()
+    check(_lib.lib().cs_model_load(_ctx(backend).handle, str(path).encode(), PRECISIONS[backend.precision],
+                                   C.byref(h)))
+    return TrainedModel(h, backend)
+
+
 @dataclass
 class EstimationResult:
     """mset.hpp:59-62"""

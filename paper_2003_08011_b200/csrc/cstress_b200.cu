@@ -73,15 +73,16 @@ struct cs_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux[2] = {nullptr, nullptr};
+  static constexpr int kSlots = 3;  // host-API pipeline depth (streams / buffer sets)
+  cudaStream_t aux[kSlots] = {nullptr, nullptr, nullptr};
   cusolverDnHandle_t solver = nullptr;
   int sm_count = 148;
   std::string name;
   // workspace (grow-only)
   DevBuf<double> wsA, wsB, wsC, wsD;
-  DevBuf<double> io_in[2], io_est[2], io_res[2];
+  DevBuf<double> io_in[kSlots], io_est[kSlots], io_res[kSlots];
   DevBuf<unsigned char> wsBytes;
-  DevBuf<float> wsX[2], wsS[2], wsXX[2];  // large-n surveillance (per stream slot): x, S operands, ||x||^2
+  DevBuf<float> wsX[kSlots], wsS[kSlots], wsXX[kSlots];  // large-n surveillance (per stream slot): x, S operands, ||x||^2
 };
 
 struct cs_model {
@@ -101,7 +102,7 @@ struct cs_model {
   DevBuf<double> D, Dn, scale, pinv;
   // FP32 tensor-core operands (precision == CS_PRECISION_FP32)
   bool tc = false;
-  int MT = 0, NB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
+  int MT = 0, NB = 1, SB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
   DevBuf<float> dn_tiles, p_tiles, dd, dn32, inv_scale, scale_f;
   float dd_max = 0.f;  // max ||D_norm(:, i)||^2 (near-zero guard prefilter)
   // large-n two-GEMM path (gemm_tc.cuh), used when the fused kernel's TMEM
@@ -291,16 +292,34 @@ void choose_tc_shape(cs_model* M) {
   // both 29.6 cycles, N=64 hits the 32-cycle M*N/256 floor), so GEMM1 tiles
   // narrower than 64 waste the tensor pipe; double buffering (NB = 2)
   // decouples the epilogue.  Then the deepest operand ring (<= 4) that fits.
-  const int pref[7][2] = {{128, 2}, {64, 2}, {128, 1}, {64, 1}, {32, 2}, {32, 1}, {16, 2}};
-  for (const auto& c : pref) {
-    const int MT = c[0], NB = c[1];
-    const int cols = tc_tmem_cols(M->N2, M->K1, MT, NB);
+  // (MT, NB, SB) in order of preference.  NB = 2 decouples GEMM1 from the
+  // similarity epilogue; measured (tools/estimate_sweep.py, timeline.py):
+  // (64,2,1) beats (64,1,1) at n = 64, but at n = 100 the only double-ACC
+  // shape that fits, (48,2,1), loses to (64,1,1) by 30% -- the narrower GEMM1
+  // (N = 48 runs at the ~30-cycle MMA floor) and the serial S buffer cost more
+  // than the GEMM1 wait it removes.
+  int pref[10][3] = {{128, 2, 2}, {64, 2, 2}, {64, 2, 1}, {128, 1, 1}, {64, 1, 1},
+                     {48, 2, 1},  {32, 2, 2}, {32, 2, 1}, {32, 1, 1}, {16, 2, 2}};
+  int npref = 10;
+  if (const char* e = std::getenv("CSB_TC_SHAPE")) {  // development override "MT,NB,SB"
+    int a = 0, b = 0, c = 0;
+    if (std::sscanf(e, "%d,%d,%d", &a, &b, &c) == 3) {
+      pref[0][0] = a;
+      pref[0][1] = b;
+      pref[0][2] = c;
+      npref = 1;
+    }
+  }
+  for (int i = 0; i < npref; ++i) {
+    const int MT = pref[i][0], NB = pref[i][1], SB = pref[i][2];
+    const int cols = tc_tmem_cols(M->N2, M->K1, MT, NB, SB);
     const size_t stage = static_cast<size_t>(2) * MT * M->K1 * 4 + static_cast<size_t>(2) * M->N2 * MT * 4;
     const size_t budget = 227 * 1024 - tc_aux_bytes(M->K1);
     const int stages = static_cast<int>(std::min<size_t>(kMaxStages, budget / stage));
     if (cols <= kTmemCols && stages >= 2) {
       M->MT = MT;
       M->NB = NB;
+      M->SB = SB;
       M->n_stages = stages;
       break;
     }
@@ -593,14 +612,17 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
     }
 #endif
   };
-  switch (M->MT * 10 + M->NB) {
-    case 1282: go(mset_estimate_tc_kernel<128, 2, IO>); break;
-    case 642: go(mset_estimate_tc_kernel<64, 2, IO>); break;
-    case 1281: go(mset_estimate_tc_kernel<128, 1, IO>); break;
-    case 641: go(mset_estimate_tc_kernel<64, 1, IO>); break;
-    case 322: go(mset_estimate_tc_kernel<32, 2, IO>); break;
-    case 321: go(mset_estimate_tc_kernel<32, 1, IO>); break;
-    case 162: go(mset_estimate_tc_kernel<16, 2, IO>); break;
+  switch (M->MT * 100 + M->NB * 10 + M->SB) {
+    case 12822: go(mset_estimate_tc_kernel<128, 2, 2, IO>); break;
+    case 6422: go(mset_estimate_tc_kernel<64, 2, 2, IO>); break;
+    case 6421: go(mset_estimate_tc_kernel<64, 2, 1, IO>); break;
+    case 4821: go(mset_estimate_tc_kernel<48, 2, 1, IO>); break;
+    case 12811: go(mset_estimate_tc_kernel<128, 1, 1, IO>); break;
+    case 6411: go(mset_estimate_tc_kernel<64, 1, 1, IO>); break;
+    case 3222: go(mset_estimate_tc_kernel<32, 2, 2, IO>); break;
+    case 3221: go(mset_estimate_tc_kernel<32, 2, 1, IO>); break;
+    case 3211: go(mset_estimate_tc_kernel<32, 1, 1, IO>); break;
+    case 1622: go(mset_estimate_tc_kernel<16, 2, 2, IO>); break;
     default: fail(CS_ERROR, "internal: bad tensor-core tile shape");
   }
 }
@@ -779,8 +801,7 @@ cs_status cs_ctx_create(int device, cs_ctx** out) {
     c->name = prop.name;
     configure_pool(device);
     CSB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
-    CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking));
-    CSB_CUDA(cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking));
+    for (auto& a : c->aux) CSB_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
     c->stream = c->own;
     *out = c.release();  // cuSOLVER handle created on the first eigendecomposition
   });
@@ -792,7 +813,7 @@ cs_status cs_ctx_destroy(cs_ctx* ctx) {
     set_device(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->solver) cusolver_api().destroy(ctx->solver);
-    for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1]})
+    for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1], ctx->aux[2]})
       if (s) cudaStreamDestroy(s);
     delete ctx;
   });
@@ -949,16 +970,21 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
     if (N == 0) return;
     const bool tc = M->precision == CS_PRECISION_FP32 && M->tc;
     const bool gm = M->precision == CS_PRECISION_FP32 && M->gemm;
-    // chunk: a multiple of the 128-observation tile, ~32 MB of input (256 MB
-    // for the two-GEMM path, whose per-launch grid needs more rows)
-    int64_t Nc = std::max<int64_t>(kObsTile, (int64_t{1} << (gm ? 25 : 22)) / std::max<int64_t>(n, 1));
+    // chunk: a multiple of the 128-observation tile.  The fused path is
+    // PCIe-bound here, so chunks are small (~8 MB in, 16 MB out) and three
+    // streams keep both copy directions busy; the two-GEMM path needs larger
+    // launches (~256 MB of input) and uses two of the slots.
+    int64_t chunk_doubles = gm ? (int64_t{1} << 25) : (int64_t{1} << 19);
+    if (const char* e = std::getenv("CSB_E2E_CHUNK_DOUBLES")) chunk_doubles = std::atoll(e);
+    int64_t Nc = std::max<int64_t>(kObsTile, chunk_doubles / std::max<int64_t>(n, 1));
     Nc = (Nc + kObsTile - 1) / kObsTile * kObsTile;
     if (!tc && !gm) Nc = std::max<int64_t>(1, std::min<int64_t>(Nc, (int64_t{1} << 27) / std::max<int64_t>(M->m, 1)));
     Nc = std::min(Nc, N);
+    const int slots = gm ? 2 : cs_ctx::kSlots;
     cudaEvent_t start;
     CSB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     CSB_CUDA(cudaEventRecord(start, ctx->stream));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < slots; ++b) {
       ctx->io_in[b].resize(Nc * n);
       ctx->io_est[b].resize(Nc * n);
       ctx->io_res[b].resize(Nc * n);
@@ -966,7 +992,7 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
     }
     int64_t chunk = 0;
     for (int64_t t0 = 0; t0 < N; t0 += Nc, ++chunk) {
-      const int b = static_cast<int>(chunk & 1);
+      const int b = static_cast<int>(chunk % slots);
       cudaStream_t st = ctx->aux[b];
       const int64_t nc = std::min(Nc, N - t0);
       CSB_CUDA(cudaMemcpy2DAsync(ctx->io_in[b].get(), nc * sizeof(double), obs + t0, N * sizeof(double),
@@ -988,8 +1014,7 @@ cs_status cs_mset_estimate(cs_ctx* ctx, const cs_model* M, const double* obs, in
                                    nc * sizeof(double), n, cudaMemcpyDeviceToHost, st));
       if (!tc && !gm) CSB_CUDA(cudaStreamSynchronize(st));  // FP64 path shares one workspace
     }
-    CSB_CUDA(cudaStreamSynchronize(ctx->aux[0]));
-    CSB_CUDA(cudaStreamSynchronize(ctx->aux[1]));
+    for (int b = 0; b < slots; ++b) CSB_CUDA(cudaStreamSynchronize(ctx->aux[b]));
     cudaEventDestroy(start);
   });
 }

@@ -90,9 +90,10 @@ constexpr int kTlCap = 8192;
   } while (0)
 #endif
 
-// TMEM columns used for a given shape and buffer count NB (1 or 2).
-__host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB) {
-  return N2 + 2 * K1 + NB * MT + NB * 2 * MT;
+// TMEM columns used for a given shape, ACC buffer count NB and S buffer
+// count SB (each 1 or 2, SB <= NB).
+__host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB, int SB) {
+  return N2 + 2 * K1 + NB * MT + SB * 2 * MT;
 }
 
 // Shared-memory footprint of everything but the operand rings: barriers,
@@ -113,12 +114,15 @@ struct Ring {
   }
 };
 
-// NB = 2: double-buffered ACC / S, two epilogue sets alternate steps, GEMM1
-//         two steps ahead.  NB = 1: single buffers, all 16 epilogue warps
-//         work on every step (4 column groups), GEMM1 one step ahead.
-template <int MT, int NB, typename IO>
+// NB = 2: double-buffered ACC, two epilogue sets alternate steps, GEMM1 two
+//         steps ahead; SB = 2 also double-buffers S, SB = 1 shares one S
+//         buffer between the sets (GEMM1 still never waits for the
+//         similarity epilogue).  NB = 1: single buffers, all 16 epilogue
+//         warps work on every step (4 column groups), GEMM1 one step ahead.
+template <int MT, int NB, int SB, typename IO>
 __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const TcParams p) {
   static_assert(NB == 1 || NB == 2, "one or two TMEM buffers");
+  static_assert(SB >= 1 && SB <= NB, "S buffers");
   constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
   constexpr int kLookahead = NB;                 // GEMM1 steps ahead of GEMM2
   constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         rd.next();
       };
       auto issue_g2 = [&](int j) {
-        const int b = NB == 2 ? (j & 1) : 0;
+        const int b = SB == 2 ? (j & 1) : 0;
         CSB_TL(1, 3, j);
         ptx::mbar_wait(&s_ready[b], s_use[b] & 1);
         ptx::mbar_wait(&p_full[rp.idx], rp.phase);
@@ -302,7 +306,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
           ah += 8;
           al += 8;
         }
-        ptx::tc_commit_elect(&s_free[b]);
+        if constexpr (SB == 1 && NB == 2) {
+          // S is free again for the set that owns the next step
+          ptx::tc_commit_elect(&s_free[j + 1 < T ? ((j + 1) & 1) : 0]);
+        } else {
+          ptx::tc_commit_elect(&s_free[b]);
+        }
         ptx::tc_commit_elect(&p_empty[rp.idx]);
         if (j == T - 1) {
           ptx::tc_commit_elect(o_full);
@@ -445,6 +454,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
     };
 
     uint32_t use = 0, tcount = 0;  // uses of this set's TMEM buffers
+    uint32_t s_waits = 0;          // SB = 1, NB = 2: waits on this set's s_free
     float xx_cur = 0.f, thr_cur = 0.f;
     auto set_thr = [&]() { thr_cur = p.tau * p.dd_max - (1.f - p.tau) * xx_cur; };
     if (static_cast<int>(blockIdx.x) < n_tiles) {
@@ -453,7 +463,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       set_thr();
     }
     const uint32_t a_base = colAcc + set * MT + c0;
-    const uint32_t s_base = colS + set * 2 * MT + c0;
+    const int sbuf = SB == 2 ? set : 0;
+    const uint32_t s_base = colS + sbuf * 2 * MT + c0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
@@ -535,10 +546,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         ptx::mbar_wait(&acc_full[set], use & 1);
         ptx::tc_fence_after();
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 11, j);
-        if constexpr (NB == 1) {
-          // single buffers: release ACC as early as possible (GEMM1 of the
+        if constexpr (SB == 1) {
+          // single S buffer: release ACC as early as possible (GEMM1 of the
           // next step may start), then wait for GEMM2 of the previous step
-          // before overwriting S
+          // before overwriting S.  With two epilogue sets sharing S, GEMM2
+          // commits to the s_free barrier of the set owning the next step, so
+          // each set counts only its own waits (a shared barrier waited on by
+          // parity is ambiguous: GEMM1 runs two steps ahead, so a set can
+          // reach its wait before the previous phase has completed).
           float vall[COLS];
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
@@ -546,7 +561,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
           if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
-          ptx::mbar_wait(&s_free[set], (use & 1) ^ 1);
+          if constexpr (NB == 1) {
+            ptx::mbar_wait(&s_free[0], (use & 1) ^ 1);
+          } else if (tcount != 0 || j != 0) {  // the CTA's first step has no predecessor
+            ptx::mbar_wait(&s_free[set], s_waits & 1);
+            ++s_waits;
+          }
           ptx::tc_fence_after();
           if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 13, j);
 #pragma unroll
@@ -569,7 +589,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         ptx::tc_fence_before();
         __syncwarp();
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 14, j);
-        if (lane == 0) ptx::mbar_arrive(&s_ready[set]);
+        if (lane == 0) ptx::mbar_arrive(&s_ready[sbuf]);
       }
       // next tile's x prologue overlaps this tile's last GEMM2
       const int next = tile + gridDim.x;

@@ -211,14 +211,17 @@ def cpu_baseline_sample(train, obs):
             "train_ms": train_s * 1e3}
 
 
-SWEEP_GRID = dict(signal_counts=[10, 20, 50, 100], observation_counts=[10_000, 100_000],
-                  memory_counts=[100, 200, 500, 1000])
-SWEEP_REPLICATES = 3
+# BASELINE configs[3] / SURVEY 8(d) C4: 7 x 3 x 6 = 126 cells, 96 admissible,
+# 5 replicates -> 480 (cell, replicate) units (~11 s on one B200)
+SWEEP_GRID = dict(signal_counts=[10, 20, 50, 100, 200, 500, 1000],
+                  observation_counts=[10_000, 100_000, 1_000_000],
+                  memory_counts=[100, 200, 500, 1000, 2000, 4000])
+SWEEP_REPLICATES = 5
 
 
 def run_bench_sweep(world, rank, local, barrier, max_over_ranks):
     """The reference's Monte Carlo scoping sweep (run_sweep, sweep.cpp:277-325)
-    on a reduced C4 grid: (cell, replicate) units LPT-placed over the ranks,
+    on the C4 grid: (cell, replicate) units LPT-placed over the ranks,
     cost records gathered over torch.distributed.  Reports units/s over the
     whole sweep wall time (device synthesis + timed train/estimate + gather),
     max over ranks."""
@@ -244,18 +247,18 @@ def run_bench_sweep(world, rank, local, barrier, max_over_ranks):
             "excluded_cells": excluded, "wall_s": wall, "timed_train_s": train_s,
             "timed_surveil_s": surv_s, "scaling": "strong", "n_gpus": world,
             "grid": {**SWEEP_GRID, "replicates": SWEEP_REPLICATES, "warmups": 1},
-            "note": "reduced C4 grid; device-side synthesis; wall includes synthesis and gather"}
+            "note": "full C4 grid (SURVEY 8d); device-side synthesis; wall includes synthesis, "
+                    "untimed warm-ups and the gather"}
 
 
 # ---------------------------------------------------------------------- B200
-def run_c3(args, local):
-    """BASELINE configs[2] (C3: n=1000, N=1M, m=4000, 16k training rows) on
-    one GPU: train time through the host API and device-resident FP32
-    surveillance on the two-GEMM tcgen05 path.  Data from the device
-    synthesiser (same recipe; host synthesis of 1e9 samples is impractical)."""
+def run_large(local, n, N, m, workload, passes=5):
+    """A large-n configuration on one GPU: train time through the device API
+    and device-resident FP32 surveillance on the two-GEMM tcgen05 path.  Data
+    from the device synthesiser (same recipe; host synthesis of 1e9+ samples
+    is impractical)."""
     import torch
     import paper_2003_08011_b200 as p
-    n, N, m = 1000, 1_000_000, 4000
     dev = torch.device("cuda", local)
     t = TEMPLATE
     base = p.cell_data_seed(MASTER_SEED, n, N, m, 0)
@@ -263,7 +266,7 @@ def run_c3(args, local):
                                                    t["kurt"], seed)
     X = p.synthesize_device(spec(TRAIN_FACTOR * m, p.derive_seed(base, [0])), local)
     backend = p.BackendId("b200", local, "fp32")
-    p.train_device(X, m, p.KernelConfig(), backend)  # warm (cuSOLVER kernels for this size)
+    p.train_device(X, m, p.KernelConfig(), backend)  # warm (pool, cuSOLVER modules for this size)
     tt = []
     for _ in range(3):
         torch.cuda.synchronize()
@@ -274,28 +277,47 @@ def run_c3(args, local):
     obs64 = p.synthesize_device(spec(N, p.derive_seed(base, [1])), local)
     obs = obs64.T.float().T          # N x n column-major FP32
     del obs64
+    torch.cuda.empty_cache()
     est = torch.empty_like(obs.T).T
     res = torch.empty_like(obs.T).T
     st = torch.cuda.current_stream(dev)
-    for _ in range(2):
-        p.estimate_device(model, obs, est, res, st)
-    steps = 5
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    p.estimate_device(model, obs, est, res, st)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(passes)]
     for a, b in ev:
         a.record(st)
         p.estimate_device(model, obs, est, res, st)
         b.record(st)
     torch.cuda.synchronize()
+    ok = bool(torch.isfinite(est).all()) and bool(torch.allclose(res, obs - est))
     ms = statistics.median(a.elapsed_time(b) for a, b in ev)
     flops = 4.0 * n * m * N
     tf32 = load_tf32_peak() or 1190.0
-    return {"workload": "C3: n=1000, N=1,000,000, m=4,000 (16k training rows), FP32 device-resident I/O",
-            "obs_per_s": N / (ms * 1e-3), "ms_per_pass": ms, "steps": steps,
+    del obs, est, res, model
+    torch.cuda.empty_cache()
+    return {"workload": workload, "n_signals": n, "n_observations": N, "n_memory": m,
+            "obs_per_s": N / (ms * 1e-3), "ms_per_pass": ms, "passes": passes,
             "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
             "frac_3xtf32": flops / (ms * 1e-3) / 1e12 / (tf32 / 3),
-            "kernels": "pack_obs + gemm3x_tf32_kernel<256,EpiSim> + gemm3x_tf32_kernel<256,EpiOut> per 32,768-observation block",
+            "kernels": "pack_obs + obs_sqnorm + gemm3x_tf32_kernel<256,EpiSim> + gemm3x_tf32_kernel<256,EpiOut> "
+                       "per observation block",
             "train_ms": statistics.median(tt) * 1e3,
-            "train_api": "cs_mset_train_device (device FP64 training rows, synchronous)"}
+            "train_api": "cs_mset_train_device (device FP64 training rows, synchronous)",
+            "outputs_checked": ok}
+
+
+def run_c3(args, local):
+    """BASELINE configs[2] (C3: n=1000, N=1M, m=4000, 16k training rows)."""
+    return run_large(local, 1000, 1_000_000, 4000,
+                     "C3: n=1000, N=1,000,000, m=4,000 (16k training rows), FP32 device-resident I/O")
+
+
+def run_c5(args, local):
+    """BASELINE configs[4] made admissible (m >= 2n, so n=4,000
+    with m=8,000) and sharded 8 ways: one GPU's shard of 10M / 8 = 1.25M
+    observations (the 8-GPU job is 8 independent shards, no collective)."""
+    return run_large(local, 4000, 1_250_000, 8000,
+                     "C5': n=4000, m=8000 (32k training rows), 1.25M observations = one of 8 shards "
+                     "of 10M, FP32 device-resident I/O", passes=3)
 
 
 def run_b200(args, world, rank, local):
@@ -326,8 +348,8 @@ def run_b200(args, world, rank, local):
 
     # ---- train (FP64), host API, synchronous: report median of 3
     train_times = []
-    model = None
-    for _ in range(3):
+    model = p.train(train, N_MEM, p.KernelConfig(), backend)  # warm (pool, cuSOLVER modules)
+    for _ in range(5):
         t0 = time.perf_counter()
         model = p.train(train, N_MEM, p.KernelConfig(), backend)
         train_times.append(time.perf_counter() - t0)
@@ -461,6 +483,8 @@ def run_b200(args, world, rank, local):
         line["sweep"] = sweep
     if world == 1 and not args.no_c3:
         line["c3"] = run_c3(args, local)
+    if world == 1 and not args.no_c5:
+        line["c5"] = run_c5(args, local)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(train, obs)
     print(json.dumps(line), flush=True)
@@ -475,6 +499,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

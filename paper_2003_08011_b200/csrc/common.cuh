@@ -86,8 +86,7 @@ struct DevBuf {
   ~DevBuf() { release(); }
   void release() {
     if (ptr) {
-      if (async) cudaFreeAsync(ptr, stream);
-      else cudaFree(ptr);
+      cudaFreeAsync(ptr, stream);
     }
     ptr = nullptr;
     count = 0;
@@ -96,16 +95,20 @@ struct DevBuf {
     if (n <= count && ptr) return;
     release();
     if (n == 0) return;
-    if (async) {
-      stream = alloc_stream();
-      CSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), stream));
-    } else {
-      CSB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
-    }
+    // every buffer comes from the device's caching pool: a plain cudaMalloc /
+    // cudaFree pair per model buffer cost 2-30 ms of page mapping and an
+    // implicit device sync per train call.  Temporaries are freed on their
+    // call's stream; long-lived (model / context) buffers on the legacy
+    // stream after their owner synchronised the device.
+    CSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), alloc_stream()));
+    // a long-lived buffer may next be used on another stream: complete the
+    // allocation before returning it (cheap when the pool has the block)
+    if (!async) CSB_CUDA(cudaStreamSynchronize(alloc_stream()));
+    stream = async ? alloc_stream() : nullptr;
     count = n;
   }
   cudaStream_t stream = nullptr;
-  bool async = false;  // stream-ordered pool allocation (call-local temporaries)
+  bool async = false;  // call-local temporary (freed stream-ordered on its call's stream)
   T* get() const { return ptr; }
 };
 

@@ -811,7 +811,7 @@ cs_status cs_ctx_destroy(cs_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
     set_device(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
+    cudaDeviceSynchronize();  // workspaces are returned to the pool below
     if (ctx->solver) cusolver_api().destroy(ctx->solver);
     for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1], ctx->aux[2]})
       if (s) cudaStreamDestroy(s);
@@ -1175,6 +1175,7 @@ cs_status cs_model_destroy(cs_model* M) {
   return guarded([&] {
     if (!M) return;
     cudaSetDevice(M->device);
+    cudaDeviceSynchronize();  // no call may still read the model's buffers
     delete M;
   });
 }

@@ -581,6 +581,8 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   p.g_coef = static_cast<float>(1.4426950408889634 / (2.0 * M->h * M->h));
   p.tau = 1.0f / 128.0f;
   p.dd_max = M->dd_max;
+  p.g2_first = 0;  // measured: GEMM2-first only helps the SB = 2 shapes marginally
+  if (const char* e = std::getenv("CSB_G2_FIRST")) p.g2_first = std::atoi(e);
   p.est = est;
   p.resid = resid;
   p.dn_stage_bytes = static_cast<uint32_t>(2 * M->MT * M->K1 * 4);

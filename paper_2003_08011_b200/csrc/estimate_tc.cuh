@@ -65,6 +65,7 @@ struct TcParams {
   void* est;
   void* resid;
   uint32_t dn_stage_bytes, p_stage_bytes;
+  int g2_first;                  // NB = 2: issue GEMM2(j) before GEMM1(j+2)
   unsigned long long* timeline;  // CSB_TIMELINE builds only: per-warp event records
 };
 
@@ -326,8 +327,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         for (int k = 0; k < prime; ++k) issue_g1(k);
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int j = 0; j < T; ++j) {
-          if (j + kLookahead < T) issue_g1(j + kLookahead);
-          issue_g2(j);
+          if (NB == 2 && p.g2_first) {
+            // two ACC buffers: GEMM2(j) first.  Queued behind GEMM1(j+2) (which
+            // waits for the similarity epilogue of step j) it would hold up the
+            // S hand-off chain; in this order the tensor pipe runs GEMM2(j-1),
+            // GEMM1(j+1), GEMM2(j), ... while the epilogue of step j overlaps.
+            issue_g2(j);
+            if (j + kLookahead < T) issue_g1(j + kLookahead);
+          } else {
+            // one ACC buffer: GEMM1(j+1) can start as soon as the epilogue
+            // has read ACC(j), before S(j) is stored
+            if (j + kLookahead < T) issue_g1(j + kLookahead);
+            issue_g2(j);
+          }
         }
         if (tile + static_cast<int>(gridDim.x) < n_tiles)
           for (int k = 0; k < prime; ++k) issue_g1(k);

@@ -126,12 +126,12 @@ def load_traffic():
         return None
 
 
-def load_tf32_peak():
-    """Dense kind::tf32 tcgen05 throughput measured on this pool by
-    tools/mma_probe (profiles/mma_probe_tf32.json), TFLOP/s at max clock."""
+def load_f16_peak():
+    """Dense kind::f16 tcgen05 throughput measured on this pool by
+    tools/mma_probe (profiles/mma_probe.json), TFLOP/s at max clock."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "mma_probe_tf32.json")))
-        return max(r["tflops_at_base_clock"] for r in d["results"])
+        d = json.load(open(os.path.join(ROOT, "profiles", "mma_probe.json")))
+        return max(r["tflops_at_base_clock"] for r in d["results"] if r["kind"] == "f16")
     except (OSError, ValueError, KeyError):
         return None
 
@@ -291,14 +291,15 @@ def run_large(local, n, N, m, workload, passes=5):
     ok = bool(torch.isfinite(est).all()) and bool(torch.allclose(res, obs - est))
     ms = statistics.median(a.elapsed_time(b) for a, b in ev)
     flops = 4.0 * n * m * N
-    tf32 = load_tf32_peak() or 1190.0
+    f16 = load_f16_peak() or 2380.0
     del obs, est, res, model
     torch.cuda.empty_cache()
     return {"workload": workload, "n_signals": n, "n_observations": N, "n_memory": m,
             "obs_per_s": N / (ms * 1e-3), "ms_per_pass": ms, "passes": passes,
             "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
-            "frac_3xtf32": flops / (ms * 1e-3) / 1e12 / (tf32 / 3),
-            "kernels": "pack_obs + obs_sqnorm + gemm3x_tf32_kernel<256,EpiSim> + gemm3x_tf32_kernel<256,EpiOut> "
+            "frac_3xf16": flops / (ms * 1e-3) / 1e12 / (f16 / 3),
+            "frac_3xf16_of_measured_bf16": flops / (ms * 1e-3) / 1e12 / (load_peaks().get("bf16_tflops", 1686.0) / 3),
+            "kernels": "pack_obs + obs_sqnorm + gemm3x_f16_kernel<256,EpiSim> + gemm3x_f16_kernel<256,EpiOut> "
                        "per observation block",
             "train_ms": statistics.median(tt) * 1e3,
             "train_api": "cs_mset_train_device (device FP64 training rows, synchronous)",
@@ -432,10 +433,10 @@ def run_b200(args, world, rank, local):
     flops_per_obs = 4.0 * N_SIG * N_MEM                       # F = 4nm
     achieved_tflops = flops_per_obs * N_OBS / (mean_ms * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops", 1590.0)
-    # tensor work actually issued: 3 TF32 products per GEMM incl. padding
-    K1, N2 = (N_SIG + 1 + 7) // 8 * 8, (N_SIG + 15) // 16 * 16
-    MT = 64  # tile the library selects for n = 100 (choose_tc_shape)
-    tf32_peak = load_tf32_peak() or bf16 / 2
+    # tensor work actually issued: 3 FP16 products per GEMM incl. padding
+    K1, N2 = (N_SIG + 1 + 15) // 16 * 16, (N_SIG + 15) // 16 * 16
+    MT = 64  # tile the library selects for n = 100 (choose_tc_shape: MT 64, 2 ACC + 2 S buffers)
+    f16_peak = load_f16_peak() or 2380.0
     m_pad = (N_MEM + MT - 1) // MT * MT
     n_tiles = (N_OBS + 127) // 128
     issued = 3 * 2 * 128 * n_tiles * m_pad * (K1 + N2)
@@ -450,7 +451,7 @@ def run_b200(args, world, rank, local):
         "config": {"workload": WORKLOAD, "n_signals": N_SIG, "n_observations_per_gpu": N_OBS,
                    "n_memory": N_MEM, "training_rows": TRAIN_FACTOR * N_MEM,
                    "kernel": "inverse_distance", "bandwidth": "sqrt(n)",
-                   "surveillance": "fused tcgen05 3xTF32 (FP32-accurate)", "train": "FP64",
+                   "surveillance": "fused tcgen05 3xFP16 (FP32-accurate, exact power-of-two operand scales)", "train": "FP64",
                    "l2": "flushed between steps (256 MiB write outside step events)",
                    "parallelism": f"dp{world} (independent observation shards)"},
         "wall_s_timed_region": wall,
@@ -466,17 +467,17 @@ def run_b200(args, world, rank, local):
                 "api": "cs_mset_estimate (pinned host FP64 in, estimates + residuals out)"},
         "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": bf16, "unit": "TFLOP/s",
                      "frac": achieved_tflops / bf16, "traffic": traffic,
-                     "kernel": "mset_estimate_tc_kernel<64,float>",
+                     "kernel": "mset_estimate_tc_kernel<64,2,2,float>",
                      "algorithmic_flops_per_launch": flops_per_obs * N_OBS,
-                     "peak_note": "peak = measured dense bf16 (MEASURED_PEAKS.json, of measured); the "
-                                  "kernel runs tcgen05 kind::tf32 (measured dense peak "
-                                  "peak_tf32_measured, tools/mma_probe) and issues 3 split "
-                                  "products per GEMM, so its algorithmic ceiling is peak_tf32/3",
-                     "peak_tf32_measured": tf32_peak,
-                     "peak_3xtf32": tf32_peak / 3,
-                     "frac_3xtf32": achieved_tflops / (tf32_peak / 3),
-                     "issued_tf32_tflops": issued_tflops,
-                     "tensor_pipe_frac_tf32": issued_tflops / tf32_peak},
+                     "peak_note": "peak = measured dense bf16 (MEASURED_PEAKS.json); the kernel runs "
+                                  "tcgen05 kind::f16 (same dense rate) and issues 3 split products per "
+                                  "GEMM (3xFP16, FP32-accurate), so its algorithmic ceiling is peak/3; "
+                                  "peak_f16_probe = tools/mma_probe at 1965 MHz",
+                     "frac_3xf16": achieved_tflops / (bf16 / 3),
+                     "peak_f16_probe": f16_peak,
+                     "frac_3xf16_of_probe": achieved_tflops / (f16_peak / 3),
+                     "issued_f16_tflops": issued_tflops,
+                     "tensor_pipe_frac_issued": issued_tflops / f16_peak},
         "clocks": clocks,
     }
     if sweep is not None:

@@ -7,6 +7,7 @@
 // /root/reference/proj.
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -82,7 +83,8 @@ struct cs_ctx {
   DevBuf<double> wsA, wsB, wsC, wsD;
   DevBuf<double> io_in[kSlots], io_est[kSlots], io_res[kSlots];
   DevBuf<unsigned char> wsBytes;
-  DevBuf<float> wsX[kSlots], wsS[kSlots], wsXX[kSlots];  // large-n surveillance (per stream slot): x, S operands, ||x||^2
+  DevBuf<__half> wsX[kSlots], wsS[kSlots];  // large-n surveillance (per stream slot): x, S operands
+  DevBuf<float> wsXX[kSlots];                // ||x||^2
 };
 
 struct cs_model {
@@ -103,13 +105,16 @@ struct cs_model {
   // FP32 tensor-core operands (precision == CS_PRECISION_FP32)
   bool tc = false;
   int MT = 0, NB = 1, SB = 1, K1 = 0, N2 = 0, m_tiles = 0, n_stages = 2;
-  DevBuf<float> dn_tiles, p_tiles, dd, dn32, inv_scale, scale_f;
+  DevBuf<__half> dn_tiles, p_tiles;  // 3xFP16 operand tiles (pack_tc.cuh)
+  DevBuf<float> dd, dn32, inv_scale, scale_f, scale_out_f;
+  DevBuf<double> p_shift, scale_out_d;  // per-signal 2^-k_s, scale_s * 2^(k_s - 14)
   float dd_max = 0.f;  // max ||D_norm(:, i)||^2 (near-zero guard prefilter)
+  float aug_x = 1.f;   // x's value in the ||d||^2 column (2^k_aug)
   // large-n two-GEMM path (gemm_tc.cuh), used when the fused kernel's TMEM
   // plan does not fit (n > ~130)
   bool gemm = false;
   int bnA = 256, ntA = 0, kcA = 0, bnB = 256, ntB = 0, kcB = 0;
-  DevBuf<float> dn_gemm, p_gemm;
+  DevBuf<__half> dn_gemm, p_gemm;
 };
 
 namespace {
@@ -284,7 +289,7 @@ bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
 
 // ------------------------------------------------------ FP32 operand packing
 void choose_tc_shape(cs_model* M) {
-  M->K1 = static_cast<int>((M->n + 1 + 7) / 8 * 8);  // + the ||d||^2 column
+  M->K1 = static_cast<int>((M->n + 1 + 15) / 16 * 16);  // + the ||d||^2 column; K = 16 per MMA
   M->N2 = static_cast<int>((M->n + 15) / 16 * 16);
   M->MT = 0;
   // (memory tile MT, TMEM buffers NB) in order of preference.  A TS-form
@@ -313,7 +318,7 @@ void choose_tc_shape(cs_model* M) {
   for (int i = 0; i < npref; ++i) {
     const int MT = pref[i][0], NB = pref[i][1], SB = pref[i][2];
     const int cols = tc_tmem_cols(M->N2, M->K1, MT, NB, SB);
-    const size_t stage = static_cast<size_t>(2) * MT * M->K1 * 4 + static_cast<size_t>(2) * M->N2 * MT * 4;
+    const size_t stage = static_cast<size_t>(2) * MT * M->K1 * 2 + static_cast<size_t>(2) * M->N2 * MT * 2;
     const size_t budget = 227 * 1024 - tc_aux_bytes(M->K1);
     const int stages = static_cast<int>(std::min<size_t>(kMaxStages, budget / stage));
     if (cols <= kTmemCols && stages >= 2) {
@@ -346,43 +351,75 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
     M->ntB = (n + M->bnB - 1) / M->bnB;
     M->kcB = m_pad / kGemmBK;
   }
-  // P = D_norm * G+  (n x m), FP64, once per model
-  TmpBuf<double> P(static_cast<size_t>(n) * m);
-  launch_gemm_exact<false, false>(st, M->Dn.get(), n, M->pinv.get(), m, n, m, m, P.get(), n);
-  if (M->tc) {
-    M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
-    M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
-    pack_dn_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->K1), 256, 0, st>>>(
-        M->Dn.get(), n, m, M->MT, M->K1, M->m_tiles, M->dn_tiles.get());
-    CSB_LAUNCH_CHECK();
-    pack_p_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->N2), 256, 0, st>>>(
-        P.get(), n, m, M->MT, M->N2, M->m_tiles, M->p_tiles.get());
-    CSB_LAUNCH_CHECK();
-  } else {
-    const size_t a_el = static_cast<size_t>(M->ntA) * M->kcA * gemm_block_floats(M->bnA);
-    const size_t b_el = static_cast<size_t>(M->ntB) * M->kcB * gemm_block_floats(M->bnB);
-    M->dn_gemm.resize(a_el);
-    M->p_gemm.resize(b_el);
-    pack_dn_gemm_kernel<<<grid_for(static_cast<int64_t>(a_el / 2)), 256, 0, st>>>(
-        M->Dn.get(), n, m, M->bnA, M->ntA, M->kcA, M->dn_gemm.get());
-    CSB_LAUNCH_CHECK();
-    pack_p_gemm_kernel<<<grid_for(static_cast<int64_t>(b_el / 2)), 256, 0, st>>>(
-        P.get(), n, m, M->bnB, M->ntB, M->kcB, M->p_gemm.get());
-    CSB_LAUNCH_CHECK();
-  }
+  // ||d||^2, FP32 D_norm, scales and max |D_norm| first: they fix the FP16
+  // operand scales (pack_tc.cuh)
   M->dd.resize(m_pad);
   M->dn32.resize(static_cast<size_t>(n) * m);
   M->inv_scale.resize(n);
   M->scale_f.resize(n);
+  TmpBuf<unsigned int> absmax(1);
+  CSB_CUDA(cudaMemsetAsync(absmax.get(), 0, sizeof(unsigned int), st));
   pack_aux_kernel<<<grid_for(std::max<int64_t>(m_pad, static_cast<int64_t>(n) * m)), 256, 0, st>>>(
       M->Dn.get(), M->scale.get(), n, m, m_pad, M->dd.get(), M->dn32.get(), M->inv_scale.get(),
-      M->scale_f.get());
+      M->scale_f.get(), absmax.get());
   CSB_LAUNCH_CHECK();
   std::vector<float> dd_host(m_pad);
+  unsigned int absmax_bits = 0;
   CSB_CUDA(cudaMemcpyAsync(dd_host.data(), M->dd.get(), m_pad * sizeof(float), cudaMemcpyDeviceToHost, st));
-  CSB_CUDA(cudaStreamSynchronize(st));  // P is freed on return
+  CSB_CUDA(cudaMemcpyAsync(&absmax_bits, absmax.get(), sizeof absmax_bits, cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
   M->dd_max = 0.f;
   for (float v : dd_host) M->dd_max = std::max(M->dd_max, v);
+  float dn_absmax;
+  std::memcpy(&dn_absmax, &absmax_bits, 4);
+  if (!(2.f * dn_absmax < kF16Safe)) {
+    // -2 d would leave the FP16 split's range (a memory vector beyond 16384
+    // standard deviations): this model surveils on the exact FP64 path
+    M->tc = false;
+    M->gemm = false;
+    return;
+  }
+  // ||d||^2 column: scale 2^-k_aug keeps it below 2^14; x carries 2^k_aug
+  int k_aug = 0;
+  if (M->dd_max > 16384.f) {
+    int ex;
+    std::frexp(static_cast<double>(M->dd_max), &ex);
+    k_aug = ex - 14;
+  }
+  const double aug_scale = std::ldexp(1.0, -k_aug);
+  M->aug_x = static_cast<float>(std::ldexp(1.0, k_aug));
+  // P = D_norm * G+  (n x m), FP64, once per model, and its
+  // per-signal power-of-two scales
+  TmpBuf<double> P(static_cast<size_t>(n) * m);
+  launch_gemm_exact<false, false>(st, M->Dn.get(), n, M->pinv.get(), m, n, m, m, P.get(), n);
+  M->p_shift.resize(n);
+  M->scale_out_d.resize(n);
+  M->scale_out_f.resize(n);
+  p_row_scale_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P.get(), M->scale.get(), n, m, M->p_shift.get(),
+                                                         M->scale_out_d.get(), M->scale_out_f.get());
+  CSB_LAUNCH_CHECK();
+  if (M->tc) {
+    M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
+    M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
+    pack_dn_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->K1), 256, 0, st>>>(
+        M->Dn.get(), n, m, M->MT, M->K1, M->m_tiles, aug_scale, M->dn_tiles.get());
+    CSB_LAUNCH_CHECK();
+    pack_p_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->N2), 256, 0, st>>>(
+        P.get(), M->p_shift.get(), n, m, M->MT, M->N2, M->m_tiles, M->p_tiles.get());
+    CSB_LAUNCH_CHECK();
+  } else {
+    const size_t a_el = static_cast<size_t>(M->ntA) * M->kcA * gemm_block_halves(M->bnA);
+    const size_t b_el = static_cast<size_t>(M->ntB) * M->kcB * gemm_block_halves(M->bnB);
+    M->dn_gemm.resize(a_el);
+    M->p_gemm.resize(b_el);
+    pack_dn_gemm_kernel<<<grid_for(static_cast<int64_t>(a_el / 2)), 256, 0, st>>>(
+        M->Dn.get(), n, m, M->bnA, M->ntA, M->kcA, aug_scale, M->dn_gemm.get());
+    CSB_LAUNCH_CHECK();
+    pack_p_gemm_kernel<<<grid_for(static_cast<int64_t>(b_el / 2)), 256, 0, st>>>(
+        P.get(), M->p_shift.get(), n, m, M->bnB, M->ntB, M->kcB, M->p_gemm.get());
+    CSB_LAUNCH_CHECK();
+  }
+  CSB_CUDA(cudaStreamSynchronize(st));  // P is freed on return
 }
 
 // ----------------------------------------------------------------- train
@@ -556,6 +593,33 @@ void estimate_fp64_device(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency)
+PFN_cuTensorMapEncodeTiled_v12000 out_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// N x n column-major FP32 output (leading dimension ld) as a 2D tensor map
+// whose box is one 128-observation tile of all n signals
+bool encode_out_map(CUtensorMap* m, void* ptr, int64_t N, int n, int64_t ld) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kObsTile), static_cast<cuuint32_t>(n)};
+  const cuuint32_t es[2] = {1, 1};
+  return out_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename IO>
 void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, int64_t N,
                int64_t ld, IO* est, IO* resid) {
@@ -574,27 +638,56 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   p.dd = M->dd.get();
   p.dn32 = M->dn32.get();
   p.inv_scale = M->inv_scale.get();
-  p.scale_f = M->scale_f.get();
-  p.scale_d = M->scale.get();
+  p.scale_f = M->scale_out_f.get();
+  p.scale_d = M->scale_out_d.get();
+  p.norm_d = M->scale.get();
+  p.aug_x = M->aug_x;
   p.kind = M->kind;
   p.inv_h = static_cast<float>(1.0 / M->h);
   p.g_coef = static_cast<float>(1.4426950408889634 / (2.0 * M->h * M->h));
   p.tau = 1.0f / 128.0f;
   p.dd_max = M->dd_max;
-  p.g2_first = 0;  // measured: GEMM2-first only helps the SB = 2 shapes marginally
-  if (const char* e = std::getenv("CSB_G2_FIRST")) p.g2_first = std::atoi(e);
   p.est = est;
   p.resid = resid;
-  p.dn_stage_bytes = static_cast<uint32_t>(2 * M->MT * M->K1 * 4);
-  p.p_stage_bytes = static_cast<uint32_t>(2 * M->N2 * M->MT * 4);
+  p.dn_stage_bytes = static_cast<uint32_t>(2 * M->MT * M->K1 * 2);  // FP16 hi | lo
+  p.p_stage_bytes = static_cast<uint32_t>(2 * M->N2 * M->MT * 2);
   p.n_stages = M->n_stages;
-  const size_t smem = M->n_stages * (static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes) +
-                      tc_aux_bytes(p.K1);
+  size_t smem = M->n_stages * (static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes) + tc_aux_bytes(p.K1);
+  // staged readout: FP32 I/O, TMA-compatible outputs (16-byte aligned,
+  // leading dimension a multiple of 4) and room for [2][n][128] FP32 next to
+  // an operand ring of >= 2 stages
+  p.staged = 0;
+  if constexpr (sizeof(IO) == 4) {
+    const size_t stage = static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes;
+    const size_t out_bytes = static_cast<size_t>(2) * M->n * kObsTile * 4;
+    const size_t budget = 227 * 1024;
+    const bool aligned = (ld % 4 == 0) && (reinterpret_cast<uintptr_t>(est) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(resid) % 16 == 0) && (est || resid);
+    const char* env = std::getenv("CSB_STAGED_READOUT");
+    const bool allow = !(env && env[0] == '0');
+    if (allow && aligned && M->n <= 256 && tc_aux_bytes(p.K1) + out_bytes + 128 + 2 * stage <= budget &&
+        out_map_encoder() != nullptr) {
+      const int ns = static_cast<int>(std::min<size_t>(
+          M->n_stages, (budget - tc_aux_bytes(p.K1) - out_bytes - 128) / stage));
+      p.n_stages = ns;
+      p.stage_out_off = static_cast<uint32_t>((ns * stage + tc_aux_bytes(p.K1) + 127) / 128 * 128);
+      smem = p.stage_out_off + out_bytes;
+      bool ok = true;
+      if (est) ok = ok && encode_out_map(&p.tmap_est, est, N, static_cast<int>(M->n), ld);
+      if (resid) ok = ok && encode_out_map(&p.tmap_res, resid, N, static_cast<int>(M->n), ld);
+      if (ok) {
+        p.staged = 1;
+      } else {
+        p.n_stages = M->n_stages;
+        smem = M->n_stages * stage + tc_aux_bytes(p.K1);
+      }
+    }
+  }
   const int tiles = static_cast<int>((N + kObsTile - 1) / kObsTile);
   const int grid = std::min(tiles, ctx->sm_count);
 #ifdef CSB_TIMELINE
-  TmpBuf<unsigned long long> tl(static_cast<size_t>(4) * kTlCap * 2);
-  CSB_CUDA(cudaMemsetAsync(tl.get(), 0, 4 * kTlCap * 2 * 8, st));
+  TmpBuf<unsigned long long> tl(static_cast<size_t>(5) * kTlCap * 2);
+  CSB_CUDA(cudaMemsetAsync(tl.get(), 0, 5 * kTlCap * 2 * 8, st));
   p.timeline = tl.get();
 #endif
   auto go = [&](auto kernel) {
@@ -603,7 +696,7 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
     kernel<<<grid, kTcThreads, smem, st>>>(p);
     CSB_LAUNCH_CHECK();
 #ifdef CSB_TIMELINE
-    std::vector<unsigned long long> h(static_cast<size_t>(4) * kTlCap * 2);
+    std::vector<unsigned long long> h(static_cast<size_t>(5) * kTlCap * 2);
     CSB_CUDA(cudaMemcpyAsync(h.data(), tl.get(), h.size() * 8, cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaStreamSynchronize(st));
     if (const char* out = std::getenv("CSB_TIMELINE_OUT")) {
@@ -636,7 +729,7 @@ void launch_gemm3x(cs_ctx* ctx, cudaStream_t st, const GemmShape& g, const Epi& 
   const int tiles = g.m_tiles * g.n_tiles;
   if (tiles == 0) return;
   const size_t smem = gemm3x_smem_bytes<BN>();
-  auto kernel = gemm3x_tf32_kernel<BN, Epi>;
+  auto kernel = gemm3x_f16_kernel<BN, Epi>;
   CSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kernel<<<std::min(tiles, ctx->sm_count), kGemmThreads, smem, st>>>(g, epi);
   CSB_LAUNCH_CHECK();
@@ -648,17 +741,17 @@ void estimate_gemm(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* ob
   if (N == 0) return;
   const int n = static_cast<int>(M->n), m = static_cast<int>(M->m);
   const int64_t m_pad = static_cast<int64_t>(M->ntA) * M->bnA;
-  // block size: S operand (8 bytes per observation x memory vector) <= 1 GiB
-  int64_t Nb = std::max<int64_t>(kGemmBM, ((int64_t{1} << 30) / (m_pad * 8)) / kGemmBM * kGemmBM);
+  // block size: S operand (FP16 hi + lo: 4 bytes per observation x memory vector) <= 1 GiB
+  int64_t Nb = std::max<int64_t>(kGemmBM, ((int64_t{1} << 30) / (m_pad * 4)) / kGemmBM * kGemmBM);
   Nb = std::min<int64_t>(Nb, (N + kGemmBM - 1) / kGemmBM * kGemmBM);
   ctx->wsX[slot].resize(static_cast<size_t>(Nb) * M->kcA * kGemmBK * 2);
-  ctx->wsS[slot].resize(static_cast<size_t>(Nb) * m_pad * 2);
+  ctx->wsS[slot].resize(static_cast<size_t>(Nb) * m_pad * 2);  // FP16 hi | lo
   ctx->wsXX[slot].resize(Nb);
   for (int64_t t0 = 0; t0 < N; t0 += Nb) {
     const int64_t nc = std::min(Nb, N - t0);
     const int mt = static_cast<int>((nc + kGemmBM - 1) / kGemmBM);
-    pack_obs_kernel<IO><<<grid_for(static_cast<int64_t>(mt) * kGemmBM * M->kcA * kGemmBK / 4), 256, 0, st>>>(
-        obs + t0, nc, ld, n, M->scale.get(), M->inv_scale.get(), M->kcA, ctx->wsX[slot].get(), nullptr);
+    pack_obs_kernel<IO><<<grid_for(static_cast<int64_t>(mt) * kGemmBM * M->kcA * kGemmBK / 8), 256, 0, st>>>(
+        obs + t0, nc, ld, n, M->scale.get(), M->inv_scale.get(), M->aug_x, M->kcA, ctx->wsX[slot].get());
     CSB_LAUNCH_CHECK();
     obs_sqnorm_kernel<IO><<<grid_for(nc), 256, 0, st>>>(obs + t0, nc, ld, n, M->scale.get(),
                                                          M->inv_scale.get(), ctx->wsXX[slot].get());
@@ -685,8 +778,8 @@ void estimate_gemm(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* ob
     const GemmShape ga{ctx->wsX[slot].get(), M->dn_gemm.get(), mt, M->ntA, M->kcA};
     if (M->bnA == 256) launch_gemm3x<256>(ctx, st, ga, es);
     else launch_gemm3x<128>(ctx, st, ga, es);
-    EpiOut<IO> eo{obs + t0, est ? est + t0 : nullptr, resid ? resid + t0 : nullptr, M->scale_f.get(),
-                  M->scale.get(), nc, ld, n};
+    EpiOut<IO> eo{obs + t0, est ? est + t0 : nullptr, resid ? resid + t0 : nullptr, M->scale_out_f.get(),
+                  M->scale_out_d.get(), nc, ld, n};
     const GemmShape gb{ctx->wsS[slot].get(), M->p_gemm.get(), mt, M->ntB, M->kcB};
     if (M->bnB == 256) launch_gemm3x<256>(ctx, st, gb, eo);
     else launch_gemm3x<128>(ctx, st, gb, eo);

@@ -13,24 +13,29 @@
 // streams the memory matrix in MT-wide tiles ("steps").  Warp roles:
 //   warp 0       producer: 1D bulk copies (TMA engine) of pre-tiled D_norm^T
 //                and P^T operand tiles into n_stages-deep shared-memory rings
-//   warp 1       MMA issuer (one thread): tcgen05.mma kind::tf32.  GEMM1 runs
-//                two steps ahead of GEMM2.
+//   warp 1       MMA issuer (one thread): tcgen05.mma kind::f16.  GEMM1 runs
+//                one or two steps ahead of GEMM2.
 //   warps 2..17  epilogue: two sets of 8 warps; set e owns the steps with
 //                j % 2 == e (and TMEM buffer e), each warp a 32-lane quarter
 //                and half of the MT columns.  All 16 warps share the x
 //                prologue and the final estimate / residual readout.
 // TMEM (512 columns x 128 lanes, lane = observation):
 //   O   [N2]            S P^T accumulator                 (GEMM2 D)
-//   X   [2 K1]          x_norm hi | lo                    (GEMM1 A, "TS" form)
-//   ACC [2 x MT]        X D_norm accumulators             (GEMM1 D)
-//   S   [2 x 2 MT]      similarity hi | lo                (GEMM2 A, "TS" form)
-// FP32-accurate products on TF32 hardware: every operand v is split into
-// hi = rna_tf32(v), lo = v - hi and each GEMM issues hi*hi + hi*lo + lo*hi
-// (3xTF32).  Single-pass TF32 misses the 1e-3 tolerance.
+//   X   [K1]            x_norm hi | lo, f16x2 pairs       (GEMM1 A, "TS" form)
+//   ACC [NB x MT]       X D_norm accumulators             (GEMM1 D)
+//   S   [SB x MT]       2^14 S hi | lo, f16x2 pairs       (GEMM2 A, "TS" form)
+// FP32-accurate products on FP16 tensor cores: every operand v is split into
+// hi = rn_f16(v), lo = rn_f16(v - hi) and each GEMM issues hi*hi + hi*lo +
+// lo*hi (3xFP16, exact power-of-two operand scales, pack_tc.cuh).  A single
+// 10-bit-mantissa pass misses the 1e-3 tolerance.  Rows holding a
+// value outside the split's safe range (|x_norm| >= 2^15) are flagged in the
+// prologue and recomputed by direct difference.
 // d2 in GEMM form cancels near zero; entries with d2 < tau (|x|^2+|d|^2) are
 // recomputed by direct difference, which keeps memory vectors
 // reproducing themselves.
 #pragma once
+
+#include <cuda.h>
 
 #include "common.cuh"
 #include "pack_tc.cuh"
@@ -40,7 +45,7 @@ namespace csb {
 
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = 32 * kEpiWarps;         // 512
-constexpr int kTcThreads = 64 + kEpiThreads;        // 576
+constexpr int kTcThreads = 96 + kEpiThreads;        // 608: producer, 2 MMA issuers, epilogue
 constexpr int kObsTile = 128;
 constexpr int kTmemCols = 512;
 constexpr int kMaxStages = 4;
@@ -50,13 +55,15 @@ struct TcParams {
   int64_t N, ld;
   int n, K1, N2, m, m_tiles;
   int n_stages;
-  const float* dn_tiles;  // m_tiles x [hi | lo] (MT x K1 canonical K-major)
-  const float* p_tiles;   // m_tiles x [hi | lo] (N2 x MT canonical K-major)
+  const __half* dn_tiles; // m_tiles x [hi | lo] (MT x K1 canonical K-major, FP16)
+  const __half* p_tiles;  // m_tiles x [hi | lo] (N2 x MT canonical K-major, FP16)
   const float* dd;        // m_tiles*MT squared norms of D_norm columns (0 padded)
   const float* dn32;      // n x m D_norm in FP32 (direct-difference recompute)
   const float* inv_scale; // n
-  const float* scale_f;   // n
-  const double* scale_d;  // n
+  const float* scale_f;   // n  estimate multipliers scale_s * 2^(k_s - 14)
+  const double* scale_d;  // n  (FP64 copy of the same)
+  const double* norm_d;   // n  signal scales (x / scale normalisation, FP64 I/O)
+  float aug_x;            // value of x's ||d||^2 column (1 / the column's scale)
   int kind;
   float inv_h;   // 1/h            (inverse distance)
   float g_coef;  // log2(e)/(2h^2) (gaussian)
@@ -65,8 +72,14 @@ struct TcParams {
   void* est;
   void* resid;
   uint32_t dn_stage_bytes, p_stage_bytes;
-  int g2_first;                  // NB = 2: issue GEMM2(j) before GEMM1(j+2)
   unsigned long long* timeline;  // CSB_TIMELINE builds only: per-warp event records
+  // staged readout (FP32 I/O when shared memory allows): estimates and
+  // residuals of a tile are written to shared memory and leave by two TMA
+  // tensor stores (an asynchronous 2 x 51 KB copy at C2 instead of a burst
+  // of 64 scalar stores per thread that stalled every CTA at the tile edge)
+  int staged;
+  uint32_t stage_out_off;  // byte offset of the [2][n][128] FP32 staging area
+  CUtensorMap tmap_est, tmap_res;
 };
 
 // Development instrumentation (tools/timeline.py): with -DCSB_TIMELINE the
@@ -94,13 +107,13 @@ constexpr int kTlCap = 8192;
 // TMEM columns used for a given shape, ACC buffer count NB and S buffer
 // count SB (each 1 or 2, SB <= NB).
 __host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB, int SB) {
-  return N2 + 2 * K1 + NB * MT + SB * 2 * MT;
+  return N2 + K1 + NB * MT + SB * MT;  // X and S as f16x2 hi | lo pairs
 }
 
 // Shared-memory footprint of everything but the operand rings: barriers,
 // staged scales and the per-row ||x||^2 partials.
 __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
-  return 512 + static_cast<size_t>(K1) * (4 + 4 + 8 + 8) + 4 * kObsTile * 4;
+  return 512 + static_cast<size_t>(K1) * (4 + 4 + 8 + 8) + 4 * kObsTile * 4 + 4 * kObsTile;
 }
 
 // ring position: (index, phase) advanced in issue order
@@ -121,11 +134,10 @@ struct Ring {
 //         similarity epilogue).  NB = 1: single buffers, all 16 epilogue
 //         warps work on every step (4 column groups), GEMM1 one step ahead.
 template <int MT, int NB, int SB, typename IO>
-__global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const TcParams p) {
+__global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const __grid_constant__ TcParams p) {
   static_assert(NB == 1 || NB == 2, "one or two TMEM buffers");
   static_assert(SB >= 1 && SB <= NB, "S buffers");
   constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
-  constexpr int kLookahead = NB;                 // GEMM1 steps ahead of GEMM2
   constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
   constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
   static_assert(COLS % 8 == 0, "epilogue column slice must be a multiple of 8");
@@ -157,6 +169,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
   float* s_inv_f = reinterpret_cast<float*>(s_scale_d + p.K1);
   float* s_scale_f = s_inv_f + p.K1;
   float* s_xx = s_scale_f + p.K1;  // [4][kObsTile]
+  uint8_t* s_bad = reinterpret_cast<uint8_t*>(s_xx + 4 * kObsTile);  // [4][kObsTile] out-of-range flags
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 16; ++i) ptx::mbar_init(&bars[i], 1);
@@ -174,7 +187,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
   }
   for (int s = threadIdx.x; s < p.K1; s += blockDim.x) {
     const bool ok = s < p.n;
-    s_inv_d[s] = ok ? 1.0 / p.scale_d[s] : 0.0;
+    s_inv_d[s] = ok ? 1.0 / p.norm_d[s] : 0.0;
     s_scale_d[s] = ok ? p.scale_d[s] : 0.0;
     s_inv_f[s] = ok ? p.inv_scale[s] : 0.f;
     s_scale_f[s] = ok ? p.scale_f[s] : 0.f;
@@ -193,9 +206,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
 
   const int K1 = p.K1, N2 = p.N2;
   const uint32_t colO = 0;
-  const uint32_t colXh = N2, colXl = N2 + K1;
-  const uint32_t colAcc = N2 + 2 * K1;   // + b*MT
-  const uint32_t colS = colAcc + NB * MT;  // + b*2MT (hi), + MT (lo)
+  const uint32_t colXh = N2, colXl = N2 + K1 / 2;
+  const uint32_t colAcc = N2 + K1;         // + b*MT
+  const uint32_t colS = colAcc + NB * MT;  // + b*MT (hi), + MT/2 (lo)
   const int n_tiles = static_cast<int>((p.N + kObsTile - 1) / kObsTile);
   const int T = p.m_tiles;
 
@@ -207,10 +220,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         // warm L2 with the next tile's observations (one 128-row segment per
         // signal column): the x prologue then reads L2, not a DRAM burst
-        // that every CTA issues at the same moment
-        const int nt = tile + gridDim.x;
-        if (nt < n_tiles) {
-          const int64_t t0 = static_cast<int64_t>(nt) * kObsTile;
+        // that every CTA issues at the same moment.  Issued at the start of
+        // the tile: the bulk prefetches share the TMA engine with the operand
+        // copies, and issuing them mid-tile (or re-warming this tile's rows
+        // for the readout) measured 17% slower.
+        auto prefetch_tile = [&](int pt) {
+          if (pt >= n_tiles) return;
+          const int64_t t0 = static_cast<int64_t>(pt) * kObsTile;
           const int64_t rows = min(static_cast<int64_t>(kObsTile), p.N - t0);
           const uintptr_t base = reinterpret_cast<uintptr_t>(p.obs);
           for (int s = lane; s < p.n; s += 32) {
@@ -218,37 +234,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
             const uintptr_t a0 = a & ~uintptr_t{15}, a1 = (a + rows * io_bytes) & ~uintptr_t{15};
             if (a1 > a0) ptx::prefetch_l2(reinterpret_cast<const void*>(a0), static_cast<uint32_t>(a1 - a0));
           }
-        }
+        };
+        prefetch_tile(tile + gridDim.x);
         for (int j = 0; j < T; ++j, r.next()) {
           CSB_TL(0, 30, j);
           ptx::mbar_wait(&dn_empty[r.idx], r.phase ^ 1);
           CSB_TL(0, 31, j);
           ptx::mbar_arrive_expect_tx_elect(&dn_full[r.idx], p.dn_stage_bytes);
           ptx::bulk_g2s_elect(dn_ring + r.idx * p.dn_stage_bytes,
-                              p.dn_tiles + static_cast<size_t>(j) * (p.dn_stage_bytes / 4),
+                              reinterpret_cast<const uint8_t*>(p.dn_tiles) + static_cast<size_t>(j) * p.dn_stage_bytes,
                               p.dn_stage_bytes, &dn_full[r.idx]);
           ptx::mbar_wait(&p_empty[r.idx], r.phase ^ 1);
           CSB_TL(0, 33, j);
           ptx::mbar_arrive_expect_tx_elect(&p_full[r.idx], p.p_stage_bytes);
           ptx::bulk_g2s_elect(p_ring + r.idx * p.p_stage_bytes,
-                              p.p_tiles + static_cast<size_t>(j) * (p.p_stage_bytes / 4),
+                              reinterpret_cast<const uint8_t*>(p.p_tiles) + static_cast<size_t>(j) * p.p_stage_bytes,
                               p.p_stage_bytes, &p_full[r.idx]);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 2) {
     // ---------------------------------------------------------- MMA issuer
     // (whole warp, converged, warp-uniform operands; one elected lane issues)
     {
-      const uint32_t idesc1 = ptx::idesc_tf32(128, MT);
-      const uint32_t idesc2 = ptx::idesc_tf32(128, N2);
+      const uint32_t idesc1 = ptx::idesc_f16(128, MT);
+      const uint32_t idesc2 = ptx::idesc_f16(128, N2);
       const uint32_t SBO = 128;
       const uint32_t LBO1 = (MT / 8) * 128;  // D_norm^T tile: MT rows x K1
       const uint32_t LBO2 = (N2 / 8) * 128;  // P^T tile: N2 rows x MT
       const uint64_t dn_desc0 = ptx::smem_desc(ptx::smem_u32(dn_ring), LBO1, SBO);
       const uint64_t p_desc0 = ptx::smem_desc(ptx::smem_u32(p_ring), LBO2, SBO);
-      const uint64_t dn_lo_off = (static_cast<uint64_t>(MT) * K1 * 4) >> 4;
-      const uint64_t p_lo_off = (static_cast<uint64_t>(N2) * MT * 4) >> 4;
+      const uint64_t dn_lo_off = (static_cast<uint64_t>(MT) * K1 * 2) >> 4;
+      const uint64_t p_lo_off = (static_cast<uint64_t>(N2) * MT * 2) >> 4;
       const uint64_t dn_stage_off = p.dn_stage_bytes >> 4, p_stage_off = p.p_stage_bytes >> 4;
       const uint64_t k_step1 = (2 * LBO1) >> 4, k_step2 = (2 * LBO2) >> 4;
       const uint32_t dO = tmem + colO;
@@ -268,10 +285,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         uint64_t bh = dn_desc0 + rd.idx * dn_stage_off;
         uint64_t bl = bh + dn_lo_off;
         uint32_t ah = tmem + colXh, al = tmem + colXl;
-        for (int kk = 0; kk < K1 / 8; ++kk) {
-          ptx::mma_tf32_ts_elect(dS, al, bh, idesc1, kk > 0 ? 1u : 0u);
-          ptx::mma_tf32_ts_elect(dS, ah, bl, idesc1, 1u);
-          ptx::mma_tf32_ts_elect(dS, ah, bh, idesc1, 1u);
+        for (int kk = 0; kk < K1 / 16; ++kk) {
+          ptx::mma_f16_ts_elect(dS, al, bh, idesc1, kk > 0 ? 1u : 0u);
+          ptx::mma_f16_ts_elect(dS, ah, bl, idesc1, 1u);
+          ptx::mma_f16_ts_elect(dS, ah, bh, idesc1, 1u);
           bh += k_step1;
           bl += k_step1;
           ah += 8;
@@ -288,22 +305,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       };
       auto issue_g2 = [&](int j) {
         const int b = SB == 2 ? (j & 1) : 0;
-        CSB_TL(1, 3, j);
+        CSB_TL(4, 3, j);
         ptx::mbar_wait(&s_ready[b], s_use[b] & 1);
         ptx::mbar_wait(&p_full[rp.idx], rp.phase);
         if (j == 0) ptx::mbar_wait(o_free, (tcount2 & 1) ^ 1);
         ptx::tc_fence_after();
-        CSB_TL(1, 4, j);
+        CSB_TL(4, 4, j);
         const uint64_t bh0 = p_desc0 + rp.idx * p_stage_off;
         const uint64_t bl0 = bh0 + p_lo_off;
-        uint32_t ah = tmem + colS + b * 2 * MT;
-        uint32_t al = ah + MT;
+        uint32_t ah = tmem + colS + b * MT;
+        uint32_t al = ah + MT / 2;
 #pragma unroll
-        for (int kk = 0; kk < MT / 8; ++kk) {
+        for (int kk = 0; kk < MT / 16; ++kk) {
           const uint64_t bh = bh0 + kk * k_step2, bl = bl0 + kk * k_step2;
-          ptx::mma_tf32_ts_elect(dO, al, bh, idesc2, (j == 0 && kk == 0) ? 0u : 1u);
-          ptx::mma_tf32_ts_elect(dO, ah, bl, idesc2, 1u);
-          ptx::mma_tf32_ts_elect(dO, ah, bh, idesc2, 1u);
+          ptx::mma_f16_ts_elect(dO, al, bh, idesc2, (j == 0 && kk == 0) ? 0u : 1u);
+          ptx::mma_f16_ts_elect(dO, ah, bl, idesc2, 1u);
+          ptx::mma_f16_ts_elect(dO, ah, bh, idesc2, 1u);
           ah += 8;
           al += 8;
         }
@@ -322,32 +339,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         rp.next();
       };
 
-      const int prime = T < kLookahead ? T : kLookahead;
-      if (static_cast<int>(blockIdx.x) < n_tiles)
-        for (int k = 0; k < prime; ++k) issue_g1(k);
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        for (int j = 0; j < T; ++j) {
-          if (NB == 2 && p.g2_first) {
-            // two ACC buffers: GEMM2(j) first.  Queued behind GEMM1(j+2) (which
-            // waits for the similarity epilogue of step j) it would hold up the
-            // S hand-off chain; in this order the tensor pipe runs GEMM2(j-1),
-            // GEMM1(j+1), GEMM2(j), ... while the epilogue of step j overlaps.
-            issue_g2(j);
-            if (j + kLookahead < T) issue_g1(j + kLookahead);
-          } else {
-            // one ACC buffer: GEMM1(j+1) can start as soon as the epilogue
-            // has read ACC(j), before S(j) is stored
-            if (j + kLookahead < T) issue_g1(j + kLookahead);
-            issue_g2(j);
-          }
-        }
-        if (tile + static_cast<int>(gridDim.x) < n_tiles)
-          for (int k = 0; k < prime; ++k) issue_g1(k);
+      // GEMM1 and GEMM2 are issued by separate warps (1 and 2), each in its
+      // own step order: GEMM1(j + NB) goes as soon as the epilogue has read
+      // ACC(j), whatever S hand-off GEMM2 is waiting on (one issuing warp
+      // serialised the two chains; tools/timeline.py).  Every commit tracks
+      // only its own warp's MMAs, and all cross-GEMM dependencies are
+      // mbarriers (ACC, S, X, O), so the tensor pipe may interleave freely.
+      if (warp == 1) {
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+          for (int j = 0; j < T; ++j) issue_g1(j);
+      } else {
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+          for (int j = 0; j < T; ++j) issue_g2(j);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;               // 0..15
+    const int ew = warp - 3;               // 0..15 (warps 3..18: every lane quarter
+                                           // appears once in each group of four)
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int set = NB == 2 ? (ew >> 3) : 0;                // step parity owned
     const int half = NB == 2 ? ((ew >> 2) & 1) : (ew >> 2);  // column slice in step
@@ -386,7 +395,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         for (int e = 0; e < 8; ++e) r[e] = obs[tt + static_cast<int64_t>(min(c * 8 + e, p.n - 1)) * p.ld];
       }
     };
-    // normalise a raw value of signal s (column n is the constant 1)
+    // normalise a raw value of signal s (column n is the constant that
+    // multiplies the packed ||d||^2 column)
     auto norm = [&](IO raw, int s, bool valid) -> float {
       float v;
       if constexpr (sizeof(IO) == 8) {
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       } else {
         v = static_cast<float>(raw) * s_inv_f[s];
       }
-      return (valid && s < p.n) ? v : (s == p.n ? 1.f : 0.f);
+      return (valid && s < p.n) ? v : (s == p.n ? p.aug_x : 0.f);
     };
 
     uint32_t prologue_count = 0;
@@ -408,6 +418,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
       float acc = 0.f;
+      bool bad = false;  // a value outside the FP16 split's range: recompute the row exactly
       bool waited = false;
       for (int k0 = g4; k0 < K1 / 8; k0 += 4 * PB) {
         float xv[PB][8];
@@ -432,16 +443,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         for (int b = 0; b < PB; ++b) {
           const int k8 = k0 + 4 * b;
           if (k8 >= K1 / 8) break;
-          uint32_t hi[8], lo[8];
+          uint32_t hi[4], lo[4];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             if (k8 * 8 + e < p.n) acc = fmaf(xv[b][e], xv[b][e], acc);
-            const uint32_t h = ptx::to_tf32(xv[b][e]);
-            hi[e] = h;
-            lo[e] = __float_as_uint(xv[b][e] - __uint_as_float(h));
+            const bool out = !(fabsf(xv[b][e]) < kF16Safe);
+            bad |= out;
+            if (out) xv[b][e] = 0.f;
           }
-          ptx::tmem_st8(tmem + lane_off + colXh + k8 * 8, hi);
-          ptx::tmem_st8(tmem + lane_off + colXl + k8 * 8, lo);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ptx::split_f16x2(xv[b][2 * e], xv[b][2 * e + 1], hi[e], lo[e]);
+          ptx::tmem_st4(tmem + lane_off + colXh + k8 * 4, hi);
+          ptx::tmem_st4(tmem + lane_off + colXl + k8 * 4, lo);
         }
       }
       if (!waited) {
@@ -450,18 +463,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         ptx::tc_fence_after();
       }
       s_xx[g4 * kObsTile + row] = acc;
+      s_bad[g4 * kObsTile + row] = bad && valid;
       ptx::tc_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       CSB_TL(2 + (ew >> 3), 22, tile);
       if (lane == 0) ptx::mbar_arrive(x_ready);
     };
+    bool bad_cur = false;  // row of the current tile recomputed exactly
     auto gather_xx = [&]() -> float {
       ptx::named_bar_sync(1, kEpiThreads);
       float xx = 0.f;
+      bool bad = false;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) xx += s_xx[g * kObsTile + row];
+      for (int g = 0; g < 4; ++g) {
+        xx += s_xx[g * kObsTile + row];
+        bad |= s_bad[g * kObsTile + row] != 0;
+      }
       ptx::named_bar_sync(1, kEpiThreads);  // partials may be overwritten afterwards
+      bad_cur = bad;
       return xx;
     };
 
@@ -476,7 +496,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
     }
     const uint32_t a_base = colAcc + set * MT + c0;
     const int sbuf = SB == 2 ? set : 0;
-    const uint32_t s_base = colS + sbuf * 2 * MT + c0;
+    const uint32_t s_base = colS + sbuf * MT + c0 / 2;  // f16x2: two columns per word
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
@@ -484,12 +504,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         const int valid_cols = min(COLS, p.m - (j * MT + c0));
         const float* dd = p.dd + static_cast<size_t>(j) * MT + c0;
         // ACC chunk c -> similarity values in v[0..CH)
-        auto compute_chunk = [&](int c, float* v) {
-          if constexpr (CH == 16) {
-            ptx::tmem_ld16_wait(tmem + lane_off + a_base + c * CH, v);
-          } else {
-            ptx::tmem_ld8_wait(tmem + lane_off + a_base + c * CH, v);
+        // the whole ACC slice of this warp: all tcgen05.ld issued, one wait
+        auto load_acc = [&](float* vall) {
+#pragma unroll
+          for (int c = 0; c < COLS / CH; ++c) {
+            if constexpr (CH == 16) {
+              ptx::tmem_ld16(tmem + lane_off + a_base + c * CH, vall + c * CH);
+            } else {
+              ptx::tmem_ld8(tmem + lane_off + a_base + c * CH, vall + c * CH);
+            }
           }
+          ptx::tc_wait_ld();
+        };
+        auto compute_chunk = [&](int c, float* v) {
           // ACC = ||d||^2 - 2 x.d (tensor core); d2 = ACC + ||x||^2.  The
           // prefilter min(ACC) < thr is a superset of the exact near-zero
           // criterion d2 < tau (||x||^2 + ||d||^2), re-checked per entry.
@@ -499,7 +526,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
             mn = fminf(mn, v[e]);
             v[e] += xx_cur;
           }
-          if (mn < thr_cur && valid) {  // rare: direct difference, not unrolled
+          if ((mn < thr_cur || bad_cur) && valid) {  // rare: direct difference, not unrolled
 #pragma unroll 1
             for (int e = 0; e < CH; ++e) {
               float cur = 0.f;
@@ -507,7 +534,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
               for (int ee = 0; ee < CH; ++ee)
                 if (ee == e) cur = v[ee];
               const int col = c * CH + e;
-              if (col >= valid_cols || !(cur < p.tau * (xx_cur + __ldg(dd + col)))) continue;
+              if (col >= valid_cols || (!bad_cur && !(cur < p.tau * (xx_cur + __ldg(dd + col))))) continue;
               const int mem = j * MT + c0 + col;
               float a = 0.f;
               for (int s = 0; s < p.n; ++s) {
@@ -538,20 +565,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
               if (c * CH + e >= valid_cols) v[e] = 0.f;
           }
         };
-        // v[0..CH) -> TMEM S hi | lo
+        // v[0..CH) -> TMEM 2^14 S hi | lo (f16x2 words)
         auto store_chunk = [&](int c, const float* v) {
 #pragma unroll
           for (int h8 = 0; h8 < CH / 8; ++h8) {
-            uint32_t hi[8], lo[8];
+            uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float sv = v[h8 * 8 + e];
-              const uint32_t h = ptx::to_tf32(sv);
-              hi[e] = h;
-              lo[e] = __float_as_uint(sv - __uint_as_float(h));
-            }
-            ptx::tmem_st8(tmem + lane_off + s_base + c * CH + h8 * 8, hi);
-            ptx::tmem_st8(tmem + lane_off + s_base + MT + c * CH + h8 * 8, lo);
+            for (int e = 0; e < 4; ++e)
+              ptx::split_f16x2(v[h8 * 8 + 2 * e] * kSScale, v[h8 * 8 + 2 * e + 1] * kSScale, hi[e], lo[e]);
+            ptx::tmem_st4(tmem + lane_off + s_base + (c * CH + h8 * 8) / 2, hi);
+            ptx::tmem_st4(tmem + lane_off + s_base + MT / 2 + (c * CH + h8 * 8) / 2, lo);
           }
         };
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 10, j);
@@ -567,11 +590,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
           // parity is ambiguous: GEMM1 runs two steps ahead, so a set can
           // reach its wait before the previous phase has completed).
           float vall[COLS];
-#pragma unroll
-          for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
+          load_acc(vall);
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
+          if (lane == 0) ptx::mbar_arrive(&acc_free[set]);  // GEMM1 may refill ACC now
+#pragma unroll
+          for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
           if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
           if constexpr (NB == 1) {
             ptx::mbar_wait(&s_free[0], (use & 1) ^ 1);
@@ -584,18 +608,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) store_chunk(c, vall + c * CH);
         } else {
-          // double buffers: S(j-2) was consumed long ago; stream chunk by chunk
+          // double buffers: read the ACC slice and release it at once (GEMM1
+          // two steps ahead overlaps the kernel map), then map and store S
+          float vall[COLS];
+          load_acc(vall);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
           ptx::mbar_wait(&s_free[set], (use & 1) ^ 1);
           ptx::tc_fence_after();
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) {
-            float v[CH];
-            compute_chunk(c, v);
-            store_chunk(c, v);
+            compute_chunk(c, vall + c * CH);
+            store_chunk(c, vall + c * CH);
           }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&acc_free[set]);  // all ACC chunks loaded
         }
         ptx::tc_wait_st();
         ptx::tc_fence_before();
@@ -610,6 +636,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       // readout: estimate = scale .* O, residual = x - estimate.  The raw
       // observations of a batch are loaded before waiting for O.
       if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
+      float* s_out = reinterpret_cast<float*>(smem + p.stage_out_off);  // [2][n][128]
+      const bool issuer = ew == 0 && lane == 0;                         // TMA store issuer
+      if (p.staged) {
+        // the previous tile's TMA stores must have read the staging area
+        if (issuer) ptx::bulk_wait_read0();
+        ptx::named_bar_sync(2, kEpiThreads);
+      }
       bool o_ready = false;
       for (int cb = g4; cb < N2 / 8; cb += 4 * PB) {
         IO xr[PB][8];
@@ -639,8 +672,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
               if (ok && resid) resid[idx] = xr[b][e] - ev;
             } else {
               const float ev = o[e] * s_scale_f[s];
-              if (ok && est) est[idx] = ev;
-              if (ok && resid) resid[idx] = xr[b][e] - ev;
+              if (p.staged) {
+                if (s < p.n) {
+                  s_out[s * kObsTile + row] = ev;
+                  s_out[(p.n + s) * kObsTile + row] = xr[b][e] - ev;
+                }
+              } else {
+                if (ok && est) est[idx] = ev;
+                if (ok && resid) resid[idx] = xr[b][e] - ev;
+              }
             }
           }
         }
@@ -649,9 +689,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
         ptx::mbar_wait(o_full, tcount & 1);
         ptx::tc_fence_after();
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(o_free);
+      if (p.staged) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(o_free);  // O read: the next tile's GEMM2 may start
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(2, kEpiThreads);
+        if (issuer) {
+          const int t0 = tile * kObsTile;
+          if (est) ptx::tma_store_2d(&p.tmap_est, t0, 0, s_out);
+          if (resid) ptx::tma_store_2d(&p.tmap_res, t0, 0, s_out + p.n * kObsTile);
+          ptx::bulk_commit();
+        }
+      }
+      if (!p.staged) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(o_free);
+      }
       if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
       if (next < n_tiles) {
         xx_cur = gather_xx();
@@ -659,6 +714,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const T
       }
       if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 26, tile);
     }
+    if (p.staged && ew == 0 && lane == 0) ptx::bulk_wait0();  // stores complete before exit
   }
   __syncthreads();
   if (warp == 0) {

@@ -18,47 +18,45 @@
 //   warp 0     producer: 1D bulk copies (TMA engine) of pre-tiled A and B
 //              operand blocks (hi | lo, canonical K-major, no swizzle) into a
 //              kStages-deep shared-memory ring
-//   warp 1     MMA issuer: per K = 8 slice three tcgen05.mma kind::tf32 (SS)
-//              -- lo.hi + hi.lo + hi.hi (3xTF32, FP32-accurate) -- into one of
-//              two TMEM accumulators (BN columns each)
+//   warp 1     MMA issuer: per K = 16 slice three tcgen05.mma kind::f16 (SS)
+//              -- lo.hi + hi.lo + hi.hi (3xFP16 with power-of-two operand
+//              scales, FP32-accurate, pack_tc.cuh) -- into one of two TMEM
+//              accumulators (BN columns each)
 //   warps 2-9  epilogue: 2 warps per TMEM lane quarter, each half of the BN
 //              columns, 16 columns per tcgen05.ld; the accumulator is released
 //              as soon as it is read, so the next tile's MMAs overlap.
 #pragma once
 
 #include "common.cuh"
+#include "pack_tc.cuh"
 #include "sm100_ptx.cuh"
 
 namespace csb {
 
 constexpr int kGemmBM = 128;      // rows (observations) per tile = TMEM lanes
-constexpr int kGemmBK = 16;       // K per pipeline stage (two k8 slices)
+constexpr int kGemmBK = 32;       // K per pipeline stage (two k16 slices)
 constexpr int kGemmStages = 4;
 constexpr int kGemmEpiWarps = 8;
 constexpr int kGemmThreads = 64 + 32 * kGemmEpiWarps;  // 320
 
-// Operand block of R rows x kGemmBK: hi then lo, canonical K-major layout.
-__host__ __device__ constexpr size_t gemm_block_floats(int R) {
+// Operand block of R rows x kGemmBK FP16 values: hi then lo, canonical
+// K-major layout (canon16).
+__host__ __device__ constexpr size_t gemm_block_halves(int R) {
   return static_cast<size_t>(2) * R * kGemmBK;
 }
 
-// element (r, k) of an R x kGemmBK canonical K-major block, in floats
-__device__ __forceinline__ int canon_idx(int r, int k, int R) {
-  return (r & 7) * 4 + (r >> 3) * 32 + (k & 3) + (k >> 2) * (R / 8) * 32;
-}
-
 struct GemmShape {
-  const float* a;  // [m_tiles][k_chunks] blocks of gemm_block_floats(BM)
-  const float* b;  // [n_tiles][k_chunks] blocks of gemm_block_floats(BN)
+  const __half* a;  // [m_tiles][k_chunks] blocks of gemm_block_halves(BM)
+  const __half* b;  // [n_tiles][k_chunks] blocks of gemm_block_halves(BN)
   int m_tiles, n_tiles, k_chunks;
 };
 
 // ------------------------------------------------------------- epilogues
 // GEMM-A: similarity map, written as GEMM-B's A operand (S hi | lo blocks).
 struct EpiSim {
-  float* s_tiles;         // [m_tiles][k_chunks_B] blocks (BM rows)
+  __half* s_tiles;        // [m_tiles][k_chunks_B] blocks (BM rows)
   int s_k_chunks;         // = padded m / kGemmBK
-  const float* xx;        // ||x_norm||^2 per observation of the block
+  const float* xx;        // ||x_norm||^2 per observation (< 0: row out of FP16 range)
   const float* dd;        // ||d_i||^2 (FP32, padded with 0)
   const float* dn32;      // n x m D_norm FP32 (direct-difference recompute)
   const void* obs;        // raw observations of the block (IO type, ld)
@@ -78,7 +76,9 @@ struct EpiSim {
   __device__ void operator()(int mt, int r, int col0, float* v) const {
     const int64_t t = static_cast<int64_t>(mt) * kGemmBM + r;
     const bool valid = t < N;
-    const float xx_r = valid ? xx[t] : 0.f;
+    const float xx_raw = valid ? xx[t] : 0.f;
+    const bool bad = xx_raw < 0.f;  // recompute every entry of the row exactly
+    const float xx_r = bad ? 0.f : xx_raw;
     const float thr = tau * dd_max - (1.f - tau) * xx_r;
     float mn = v[0];
 #pragma unroll
@@ -86,7 +86,7 @@ struct EpiSim {
       mn = fminf(mn, v[e]);
       v[e] += xx_r;
     }
-    if (mn < thr && valid) {  // rare: exact near-zero criterion + direct difference
+    if ((mn < thr || bad) && valid) {  // rare: exact near-zero criterion + direct difference
 #pragma unroll 1
       for (int e = 0; e < 16; ++e) {
         float cur = 0.f;
@@ -94,7 +94,7 @@ struct EpiSim {
         for (int ee = 0; ee < 16; ++ee)
           if (ee == e) cur = v[ee];
         const int col = col0 + e;
-        if (col >= m || !(cur < tau * (xx_r + __ldg(dd + col)))) continue;
+        if (col >= m || (!bad && !(cur < tau * (xx_r + __ldg(dd + col))))) continue;
         float a = 0.f;
         for (int s = 0; s < n; ++s) {
           const float d = xnorm(t, s) - __ldg(dn32 + static_cast<size_t>(col) * n + s);
@@ -120,23 +120,21 @@ struct EpiSim {
       for (int e = 0; e < 16; ++e)
         if (col0 + e >= m) v[e] = 0.f;
     }
-    // col0 is a multiple of 16 = kGemmBK: the 16 values are one K-chunk row
-    float* blk = s_tiles + (static_cast<size_t>(mt) * s_k_chunks + col0 / kGemmBK) * gemm_block_floats(kGemmBM);
+    // col0 is a multiple of 16: the 16 values are half a K-chunk row, two
+    // 8-value core-matrix rows of 16 bytes (2^14 S, FP16 hi | lo)
+    __half* blk = s_tiles + (static_cast<size_t>(mt) * s_k_chunks + col0 / kGemmBK) * gemm_block_halves(kGemmBM);
+    const int kk0 = col0 % kGemmBK;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float4 hi, lo;
-      float* h = &hi.x;
-      float* l = &lo.x;
+    for (int q = 0; q < 2; ++q) {
+      uint4 hi, lo;
+      uint32_t* h = &hi.x;
+      uint32_t* l = &lo.x;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float sv = v[4 * q + e];
-        const float hv = __uint_as_float(ptx::to_tf32(sv));
-        h[e] = hv;
-        l[e] = sv - hv;
-      }
-      const int off = canon_idx(r, 4 * q, kGemmBM);
-      *reinterpret_cast<float4*>(blk + off) = hi;
-      *reinterpret_cast<float4*>(blk + kGemmBM * kGemmBK + off) = lo;
+      for (int e = 0; e < 4; ++e)
+        ptx::split_f16x2(v[8 * q + 2 * e] * kSScale, v[8 * q + 2 * e + 1] * kSScale, h[e], l[e]);
+      const size_t off = canon16(r, kk0 + 8 * q, kGemmBM);
+      *reinterpret_cast<uint4*>(blk + off) = hi;
+      *reinterpret_cast<uint4*>(blk + kGemmBM * kGemmBK + off) = lo;
     }
   }
 };
@@ -183,10 +181,10 @@ struct EpiOut {
 
 // ------------------------------------------------------------ the kernel
 template <int BN, class Epi>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_tf32_kernel(const GemmShape g, const Epi epi) {
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_f16_kernel(const GemmShape g, const Epi epi) {
   static_assert(BN == 128 || BN == 256, "BN");
-  constexpr uint32_t kABytes = gemm_block_floats(kGemmBM) * 4;
-  constexpr uint32_t kBBytes = gemm_block_floats(BN) * 4;
+  constexpr uint32_t kABytes = gemm_block_halves(kGemmBM) * 2;
+  constexpr uint32_t kBBytes = gemm_block_halves(BN) * 2;
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / 32, 0);
@@ -230,14 +228,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_tf32_kernel(const Gemm
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       int mt, nt;
       coords(tile, mt, nt);
-      const float* a = g.a + static_cast<size_t>(mt) * KC * gemm_block_floats(kGemmBM);
-      const float* b = g.b + static_cast<size_t>(nt) * KC * gemm_block_floats(BN);
+      const __half* a = g.a + static_cast<size_t>(mt) * KC * gemm_block_halves(kGemmBM);
+      const __half* b = g.b + static_cast<size_t>(nt) * KC * gemm_block_halves(BN);
       for (int kc = 0; kc < KC; ++kc) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* dst = smem + stage * kStageBytes;
         ptx::mbar_arrive_expect_tx_elect(&full[stage], kStageBytes);
-        ptx::bulk_g2s_elect(dst, a + static_cast<size_t>(kc) * gemm_block_floats(kGemmBM), kABytes, &full[stage]);
-        ptx::bulk_g2s_elect(dst + kABytes, b + static_cast<size_t>(kc) * gemm_block_floats(BN), kBBytes,
+        ptx::bulk_g2s_elect(dst, a + static_cast<size_t>(kc) * gemm_block_halves(kGemmBM), kABytes, &full[stage]);
+        ptx::bulk_g2s_elect(dst + kABytes, b + static_cast<size_t>(kc) * gemm_block_halves(BN), kBBytes,
                             &full[stage]);
         if (++stage == kGemmStages) {
           stage = 0;
@@ -246,7 +244,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_tf32_kernel(const Gemm
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = ptx::idesc_tf32(kGemmBM, BN);
+    const uint32_t idesc = ptx::idesc_f16(kGemmBM, BN);
     constexpr uint32_t LBO_A = (kGemmBM / 8) * 128, LBO_B = (BN / 8) * 128;
     const uint32_t s0 = ptx::smem_u32(smem);
     uint32_t stage = 0, phase = 0, local = 0;
@@ -260,14 +258,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_tf32_kernel(const Gemm
         ptx::tc_fence_after();
         const uint32_t sa = s0 + stage * kStageBytes, sb = sa + kABytes;
 #pragma unroll
-        for (int k8 = 0; k8 < kGemmBK / 8; ++k8) {
-          const uint64_t ah = ptx::smem_desc(sa + k8 * 2 * LBO_A, LBO_A, 128);
-          const uint64_t al = ptx::smem_desc(sa + kABytes / 2 + k8 * 2 * LBO_A, LBO_A, 128);
-          const uint64_t bh = ptx::smem_desc(sb + k8 * 2 * LBO_B, LBO_B, 128);
-          const uint64_t bl = ptx::smem_desc(sb + kBBytes / 2 + k8 * 2 * LBO_B, LBO_B, 128);
-          ptx::mma_tf32_ss_elect(d, al, bh, idesc, (kc | k8) != 0);
-          ptx::mma_tf32_ss_elect(d, ah, bl, idesc, 1u);
-          ptx::mma_tf32_ss_elect(d, ah, bh, idesc, 1u);
+        for (int k16 = 0; k16 < kGemmBK / 16; ++k16) {
+          const uint64_t ah = ptx::smem_desc(sa + k16 * 2 * LBO_A, LBO_A, 128);
+          const uint64_t al = ptx::smem_desc(sa + kABytes / 2 + k16 * 2 * LBO_A, LBO_A, 128);
+          const uint64_t bh = ptx::smem_desc(sb + k16 * 2 * LBO_B, LBO_B, 128);
+          const uint64_t bl = ptx::smem_desc(sb + kBBytes / 2 + k16 * 2 * LBO_B, LBO_B, 128);
+          ptx::mma_f16_ss_elect(d, al, bh, idesc, (kc | k16) != 0);
+          ptx::mma_f16_ss_elect(d, ah, bl, idesc, 1u);
+          ptx::mma_f16_ss_elect(d, ah, bh, idesc, 1u);
         }
         ptx::tc_commit_elect(&empty[stage]);
         if (++stage == kGemmStages) {
@@ -312,57 +310,61 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm3x_tf32_kernel(const Gemm
 
 template <int BN>
 constexpr size_t gemm3x_smem_bytes() {
-  return kGemmStages * (gemm_block_floats(kGemmBM) + gemm_block_floats(BN)) * 4 + 256;
+  return kGemmStages * (gemm_block_halves(kGemmBM) + gemm_block_halves(BN)) * 2 + 256;
 }
 
 // ------------------------------------------------------------- packing
-// Observation block -> GEMM-A operand: x_norm = x / scale augmented with a
-// constant 1 at column n, split hi | lo; ||x_norm||^2 per observation.
-// One thread per (observation, 4 consecutive K).
+// Observation block -> GEMM-A operand: x_norm = x / scale augmented with
+// aug_x at column n, split into FP16 hi | lo; values outside the split's
+// range are zeroed (their rows are recomputed exactly, see obs_sqnorm).
+// One thread per (observation, 8 consecutive K): 16-byte stores.
 template <typename IO>
 __global__ void pack_obs_kernel(const IO* __restrict__ obs, int64_t N, int64_t ld, int n,
                                 const double* __restrict__ scale_d, const float* __restrict__ inv_scale_f,
-                                int k_chunks, float* __restrict__ tiles, float* __restrict__ xx) {
+                                float aug_x, int k_chunks, __half* __restrict__ tiles) {
   const int m_tiles = static_cast<int>((N + kGemmBM - 1) / kGemmBM);
   const int64_t rows = static_cast<int64_t>(m_tiles) * kGemmBM;
-  const int kq = k_chunks * kGemmBK / 4;
-  const int64_t total = rows * kq;
+  const int k8n = k_chunks * kGemmBK / 8;
+  const int64_t total = rows * k8n;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t t = e % rows;
-    const int k4 = static_cast<int>(e / rows);
-    float4 hi, lo;
-    float* h = &hi.x;
-    float* l = &lo.x;
+    const int k8 = static_cast<int>(e / rows);
+    float v[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int s = 4 * k4 + i;
-      float v = 0.f;
+    for (int i = 0; i < 8; ++i) {
+      const int s = 8 * k8 + i;
+      float x = 0.f;
       if (t < N) {
         if (s < n) {
           if constexpr (sizeof(IO) == 8) {
-            v = static_cast<float>(static_cast<double>(obs[t + s * ld]) / scale_d[s]);
+            x = static_cast<float>(static_cast<double>(obs[t + s * ld]) / scale_d[s]);
           } else {
-            v = static_cast<float>(obs[t + s * ld]) * inv_scale_f[s];
+            x = static_cast<float>(obs[t + s * ld]) * inv_scale_f[s];
           }
+          if (!(fabsf(x) < kF16Safe)) x = 0.f;
         } else if (s == n) {
-          v = 1.f;
+          x = aug_x;
         }
       }
-      const float hv = __uint_as_float(ptx::to_tf32(v));
-      h[i] = hv;
-      l[i] = v - hv;
+      v[i] = x;
     }
+    uint4 hi, lo;
+    uint32_t* h = &hi.x;
+    uint32_t* l = &lo.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ptx::split_f16x2(v[2 * i], v[2 * i + 1], h[i], l[i]);
     const int mt = static_cast<int>(t / kGemmBM), r = static_cast<int>(t % kGemmBM);
-    const int kc = (4 * k4) / kGemmBK, kk = (4 * k4) % kGemmBK;
-    float* blk = tiles + (static_cast<size_t>(mt) * k_chunks + kc) * gemm_block_floats(kGemmBM);
-    const int off = canon_idx(r, kk, kGemmBM);
-    *reinterpret_cast<float4*>(blk + off) = hi;
-    *reinterpret_cast<float4*>(blk + kGemmBM * kGemmBK + off) = lo;
+    const int kc = (8 * k8) / kGemmBK, kk = (8 * k8) % kGemmBK;
+    __half* blk = tiles + (static_cast<size_t>(mt) * k_chunks + kc) * gemm_block_halves(kGemmBM);
+    const size_t off = canon16(r, kk, kGemmBM);
+    *reinterpret_cast<uint4*>(blk + off) = hi;
+    *reinterpret_cast<uint4*>(blk + kGemmBM * kGemmBK + off) = lo;
   }
 }
 
-// ||x_norm||^2 per observation (FP32, sequential over signals)
+// ||x_norm||^2 per observation (FP32, sequential over signals); -1 marks a
+// row with a value outside the FP16 split's range
 template <typename IO>
 __global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t ld, int n,
                                   const double* __restrict__ scale_d, const float* __restrict__ inv_scale_f,
@@ -371,7 +373,7 @@ __global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     // sequential sum over signals (deterministic); eight independent loads
     // in flight per step
-    float a = 0.f;
+    float a = 0.f, mx = 0.f;
     int s = 0;
     for (; s + 8 <= n; s += 8) {
       IO r[8];
@@ -385,6 +387,7 @@ __global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t
           v = static_cast<float>(r[e]) * inv_scale_f[s + e];
         }
         a = fmaf(v, v, a);
+        mx = fmaxf(mx, fabsf(v));
       }
     }
     for (; s < n; ++s) {
@@ -395,15 +398,17 @@ __global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t
         v = static_cast<float>(obs[t + s * ld]) * inv_scale_f[s];
       }
       a = fmaf(v, v, a);
+      mx = fmaxf(mx, fabsf(v));
     }
-    xx[t] = a;
+    xx[t] = (mx < kF16Safe) ? a : -1.f;
   }
 }
 
 // Model operand for GEMM-A's B side: rows = memory vectors (BN-row tiles),
-// K = signals + the ||d||^2 column; -2 D_norm (exact) and ||d||^2 in FP64.
+// K = signals + the ||d||^2 column: -2 D_norm (exact) and ||d||^2 * aug_scale
+// (FP64), FP16 hi | lo.
 __global__ void pack_dn_gemm_kernel(const double* __restrict__ Dn, int n, int m, int BN, int n_tiles,
-                                    int k_chunks, float* __restrict__ out) {
+                                    int k_chunks, double aug_scale, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(BN) * kGemmBK;
   const int64_t total = per * k_chunks * n_tiles;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -422,21 +427,22 @@ __global__ void pack_dn_gemm_kernel(const double* __restrict__ Dn, int n, int m,
           const double d = Dn[s + static_cast<int64_t>(mem) * n];
           v = fma(d, d, v);
         }
+        v *= aug_scale;
       }
     }
-    const float hv = __uint_as_float(ptx::to_tf32(static_cast<float>(v)));
-    const float lv = static_cast<float>(v - static_cast<double>(hv));
-    float* o = out + blk * 2 * per;
-    const int off = (r & 7) * 4 + (r >> 3) * 32 + (kk & 3) + (kk >> 2) * (BN / 8) * 32;
-    o[off] = hv;
-    o[per + off] = lv;
+    __half hv, lv;
+    split_f16(v, hv, lv);
+    __half* o = out + blk * 2 * per;
+    o[canon16(r, kk, BN)] = hv;
+    o[per + canon16(r, kk, BN)] = lv;
   }
 }
 
 // Model operand for GEMM-B's B side: rows = signals (BN-row tiles), K =
-// memory vectors (padded to k_chunks * kGemmBK); P = D_norm G+ (FP64).
-__global__ void pack_p_gemm_kernel(const double* __restrict__ P, int n, int m, int BN, int n_tiles,
-                                   int k_chunks, float* __restrict__ out) {
+// memory vectors (padded to k_chunks * kGemmBK); P = D_norm G+ (FP64), row s
+// scaled by p_shift[s].
+__global__ void pack_p_gemm_kernel(const double* __restrict__ P, const double* __restrict__ p_shift, int n,
+                                   int m, int BN, int n_tiles, int k_chunks, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(BN) * kGemmBK;
   const int64_t total = per * k_chunks * n_tiles;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -446,13 +452,12 @@ __global__ void pack_p_gemm_kernel(const double* __restrict__ P, int n, int m, i
     const int nt = static_cast<int>(blk / k_chunks), kc = static_cast<int>(blk % k_chunks);
     const int r = rem % BN, kk = rem / BN;
     const int sig = nt * BN + r, mem = kc * kGemmBK + kk;
-    const double v = (sig < n && mem < m) ? P[sig + static_cast<int64_t>(mem) * n] : 0.0;
-    const float hv = __uint_as_float(ptx::to_tf32(static_cast<float>(v)));
-    const float lv = static_cast<float>(v - static_cast<double>(hv));
-    float* o = out + blk * 2 * per;
-    const int off = (r & 7) * 4 + (r >> 3) * 32 + (kk & 3) + (kk >> 2) * (BN / 8) * 32;
-    o[off] = hv;
-    o[per + off] = lv;
+    const double v = (sig < n && mem < m) ? P[sig + static_cast<int64_t>(mem) * n] * p_shift[sig] : 0.0;
+    __half hv, lv;
+    split_f16(v, hv, lv);
+    __half* o = out + blk * 2 * per;
+    o[canon16(r, kk, BN)] = hv;
+    o[per + canon16(r, kk, BN)] = lv;
   }
 }
 

@@ -1,23 +1,45 @@
-// pack_tc.cuh -- one-time (train) pre-tiling of the FP32 tensor-core operands.
+// pack_tc.cuh -- one-time (train) packing of the tensor-core operands.
+//
+// Surveillance runs its two products as 3xFP16 on tcgen05 kind::f16: every
+// operand v is split into hi = rn_f16(v) and lo = rn_f16(v - hi) (an 11 + 11
+// bit mantissa, the same as the 3xTF32 split but half the bytes and twice the
+// MMA rate), and each GEMM issues lo.hi + hi.lo + hi.hi into one FP32
+// accumulator.  FP16's exponent range is handled with exact power-of-two
+// scales: the ||d||^2 column by 2^-k_aug (x carries 2^k_aug in the matching
+// column), the similarity S by 2^14, and every row of P = D_norm G+ by
+// 2^-k_s so that max |P(s, :)| < 2^14; the estimate epilogue multiplies by
+// scale_s * 2^(k_s - 14).  Numerics (numpy emulation of the exact split and
+// FP32 accumulation): max relative estimate error 5e-7 .. 5e-6 on the SURVEY
+// H1 shapes, the same as 3xTF32.
 #pragma once
+
+#include <cuda_fp16.h>
 
 #include "sm100_ptx.cuh"
 
 namespace csb {
 
-// Operand pre-tiling (once per model, at train time).  Canonical K-major,
-// no-swizzle layout: element (r, k) of an R x K block sits at byte
-//   (r%8)*16 + (r/8)*128 + (k%4)*4 + (k/4)*LBO,  LBO = (R/8)*128.
-__device__ __forceinline__ size_t canon_off(int r, int k, int R) {
-  return static_cast<size_t>((r & 7) * 4 + (r >> 3) * 32 + (k & 3) + (k >> 2) * (R / 8) * 32);
+constexpr float kSScale = 16384.f;  // 2^14: S in (0, 1] -> normal FP16 range
+constexpr float kF16Safe = 32768.f;  // |operand| >= this is outside the split's safe range
+
+// Canonical K-major, no-swizzle layout of an R x K block of 16-bit
+// elements: core matrices of 8 rows x 16 bytes; element (r, k) at
+//   (r%8)*16 + (r/8)*128 + (k%8)*2 + (k/8)*LBO bytes,  LBO = (R/8)*128.
+__host__ __device__ __forceinline__ size_t canon16(int r, int k, int R) {
+  return static_cast<size_t>((r & 7) * 8 + (r >> 3) * 64 + (k & 7) + (k >> 3) * (R / 8) * 64);
 }
 
-// D_norm^T tiles: block j holds memory vectors j*MT.. as rows, signals as K,
-// pre-scaled for the GEMM-form distance: column k < n holds -2 d_k (exact),
-// column n holds ||d||^2 (FP64, split) -- with x augmented by a constant 1 in
-// column n, GEMM1 yields ||d||^2 - 2 x.d directly (one FADD of ||x||^2 left).
+__device__ __forceinline__ void split_f16(double v, __half& hi, __half& lo) {
+  hi = __double2half(v);
+  lo = __double2half(v - static_cast<double>(__half2float(hi)));
+}
+
+// D_norm^T tiles: block j holds memory vectors j*MT.. as rows, signals as K:
+// column k < n holds -2 d_k (exact), column n holds ||d||^2 * aug_scale
+// (FP64, split) -- with x augmented by 1/aug_scale in column n, GEMM1 yields
+// ||d||^2 - 2 x.d directly (one FADD of ||x||^2 left).
 __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m, int MT, int K1,
-                                     int m_tiles, float* __restrict__ out) {
+                                     int m_tiles, double aug_scale, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(MT) * K1;
   const int64_t total = per * m_tiles;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -35,20 +57,21 @@ __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m
           const double d = Dn[s + static_cast<int64_t>(mem) * n];
           v = fma(d, d, v);
         }
+        v *= aug_scale;
       }
     }
-    const float f = static_cast<float>(v);
-    const float hi = __uint_as_float(ptx::to_tf32(f));
-    const float lo = static_cast<float>(v - static_cast<double>(hi));
-    float* blk = out + static_cast<size_t>(j) * 2 * per;
-    blk[canon_off(r, k, MT)] = hi;
-    blk[per + canon_off(r, k, MT)] = lo;
+    __half hi, lo;
+    split_f16(v, hi, lo);
+    __half* blk = out + static_cast<size_t>(j) * 2 * per;
+    blk[canon16(r, k, MT)] = hi;
+    blk[per + canon16(r, k, MT)] = lo;
   }
 }
 
-// P^T tiles: block j holds signals as rows (N2), memory vectors j*MT.. as K.
-__global__ void pack_p_tiles_kernel(const double* __restrict__ P, int n, int m, int MT, int N2,
-                                    int m_tiles, float* __restrict__ out) {
+// P^T tiles: block j holds signals as rows (N2), memory vectors j*MT.. as K;
+// row s scaled by p_shift[s] = 2^-k_s.
+__global__ void pack_p_tiles_kernel(const double* __restrict__ P, const double* __restrict__ p_shift, int n,
+                                    int m, int MT, int N2, int m_tiles, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(N2) * MT;
   const int64_t total = per * m_tiles;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -57,21 +80,44 @@ __global__ void pack_p_tiles_kernel(const double* __restrict__ P, int n, int m, 
     const int rem = static_cast<int>(e % per);
     const int r = rem % N2, k = rem / N2;
     const int mem = j * MT + k;
-    const double v = (r < n && mem < m) ? P[r + static_cast<int64_t>(mem) * n] : 0.0;
-    const float f = static_cast<float>(v);
-    const float hi = __uint_as_float(ptx::to_tf32(f));
-    const float lo = static_cast<float>(v - static_cast<double>(hi));
-    float* blk = out + static_cast<size_t>(j) * 2 * per;
-    blk[canon_off(r, k, N2)] = hi;
-    blk[per + canon_off(r, k, N2)] = lo;
+    const double v = (r < n && mem < m) ? P[r + static_cast<int64_t>(mem) * n] * p_shift[r] : 0.0;
+    __half hi, lo;
+    split_f16(v, hi, lo);
+    __half* blk = out + static_cast<size_t>(j) * 2 * per;
+    blk[canon16(r, k, N2)] = hi;
+    blk[per + canon16(r, k, N2)] = lo;
   }
 }
 
-// ||D_norm(:, c)||^2 (FP64 -> FP32, zero padded), D_norm in FP32, 1/scale.
+// Per signal s: p_shift = 2^-k_s with max |P(s, :)| * 2^-k_s in [2^13, 2^14)
+// (1 for an all-zero row), and the estimate multipliers
+// scale_out = scale_s * 2^(k_s - 14) in FP64 and FP32 (exact power-of-two
+// rescaling of the FP64 scale).
+__global__ void p_row_scale_kernel(const double* __restrict__ P, const double* __restrict__ scale, int n, int m,
+                                   double* __restrict__ p_shift, double* __restrict__ scale_out_d,
+                                   float* __restrict__ scale_out_f) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double mx = 0.0;
+  for (int i = 0; i < m; ++i) mx = fmax(mx, fabs(P[s + static_cast<int64_t>(i) * n]));
+  int k = 0;
+  if (mx > 0.0) {
+    int ex;
+    frexp(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+    k = ex - 14;     // mx * 2^-k in [2^13, 2^14)
+  }
+  p_shift[s] = ldexp(1.0, -k);
+  scale_out_d[s] = ldexp(scale[s], k) / static_cast<double>(kSScale);
+  scale_out_f[s] = static_cast<float>(scale_out_d[s]);
+}
+
+// ||D_norm(:, c)||^2 (FP64 -> FP32, zero padded), D_norm in FP32, 1/scale,
+// and max |D_norm| (as the bit pattern of a non-negative float, for the
+// FP16-range check of the -2 d operand).
 __global__ void pack_aux_kernel(const double* __restrict__ Dn, const double* __restrict__ scale,
                                 int n, int m, int m_pad, float* __restrict__ dd,
                                 float* __restrict__ dn32, float* __restrict__ inv_scale,
-                                float* __restrict__ scale_f) {
+                                float* __restrict__ scale_f, unsigned int* __restrict__ dn_absmax) {
   const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t c = tid; c < m_pad; c += stride) {
@@ -83,12 +129,16 @@ __global__ void pack_aux_kernel(const double* __restrict__ Dn, const double* __r
       }
     dd[c] = static_cast<float>(a);
   }
-  for (int64_t e = tid; e < static_cast<int64_t>(n) * m; e += stride) dn32[e] = static_cast<float>(Dn[e]);
+  float mx = 0.f;
+  for (int64_t e = tid; e < static_cast<int64_t>(n) * m; e += stride) {
+    dn32[e] = static_cast<float>(Dn[e]);
+    mx = fmaxf(mx, fabsf(dn32[e]));
+  }
+  if (mx > 0.f) atomicMax(dn_absmax, __float_as_uint(mx));
   for (int64_t s = tid; s < n; s += stride) {
     inv_scale[s] = static_cast<float>(1.0 / scale[s]);
     scale_f[s] = static_cast<float>(scale[s]);
   }
 }
-
 
 }  // namespace csb

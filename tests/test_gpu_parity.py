@@ -370,3 +370,31 @@ def test_cpp_host_layer_on_gpu(p):
     r = subprocess.run([b.build_cpp_test()], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,m,N", [(100, 1000, 1000), (20, 100, 4000), (64, 512, 3000), (33, 70, 1024)])
+def test_staged_readout_matches_direct_stores(p, oracle, n, m, N):
+    """FP32 device I/O: the TMA-staged readout (estimates and residuals leave
+    through shared memory and two tensor stores per tile, partial last tile
+    included) is bitwise the direct-store path."""
+    import os
+    import torch
+    X = oracle.synthesize_uniform(n, 4 * m, 0.5, 0.3, 1.0, 0.5, 4.0, 5 + n)
+    obs = oracle.synthesize_uniform(n, N, 0.5, 0.3, 1.0, 0.5, 4.0, 6 + n)
+    g = p.train(X, m, p.KernelConfig(), B(p, "fp32"))
+    d_obs = torch.tensor(obs.T.copy(), dtype=torch.float32, device="cuda").T
+    out = {}
+    for staged in ("1", "0"):
+        os.environ["CSB_STAGED_READOUT"] = staged
+        try:
+            e = torch.full_like(d_obs.T, float("nan")).T
+            r = torch.full_like(d_obs.T, float("nan")).T
+            p.estimate_device(g, d_obs, e, r)
+            torch.cuda.synchronize()
+            out[staged] = (e.cpu().numpy(), r.cpu().numpy())
+        finally:
+            del os.environ["CSB_STAGED_READOUT"]
+    assert np.isfinite(out["1"][0]).all() and np.isfinite(out["1"][1]).all()
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+    want = p.estimate(g, obs).estimates
+    assert rel(out["1"][0].astype(np.float64), want) <= 1e-5

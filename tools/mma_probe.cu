@@ -17,8 +17,8 @@
 using namespace csb;
 
 __device__ __forceinline__ uint32_t idesc(int kind, int M, int N) {
-  // kind 0: tf32 (a/b format 2), kind 1: bf16 (format 1); F32 accumulate
-  const uint32_t f = kind == 0 ? 2u : 1u;
+  // kind 0: tf32 (a/b format 2), kind 1: f16 (kind::f16, format 0); F32 accumulate
+  const uint32_t f = kind == 0 ? 2u : 0u;
   return (1u << 4) | (f << 7) | (f << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
 }
@@ -58,14 +58,17 @@ __global__ void __launch_bounds__(128, 1) probe(int kind, int ts, int N, int ite
     const uint64_t bdesc = ptx::smem_desc(sb, (N / 8) * 128, 128);
     const uint64_t adesc = ptx::smem_desc(sb + 32768, 16 * 128, 128);
     const long long t0 = clock64();
-    if (ts) {
-      for (int i = 0; i < iters; ++i) ptx::mma_tf32_ts_elect(tmem, tmem + 256 + (i & 7) * 8, bdesc, id, 1u);
+    if (kind == 0) {
+      if (ts) {
+        for (int i = 0; i < iters; ++i) ptx::mma_tf32_ts_elect(tmem, tmem + 256 + (i & 7) * 8, bdesc, id, 1u);
+      } else {
+        for (int i = 0; i < iters; ++i) ptx::mma_tf32_ss_elect(tmem, adesc, bdesc, id, 1u);
+      }
     } else {
-      for (int i = 0; i < iters; ++i) {
-        asm volatile(
-            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t}" ::"r"(tmem),
-            "l"(adesc), "l"(bdesc), "r"(id));
+      if (ts) {
+        for (int i = 0; i < iters; ++i) ptx::mma_f16_ts_elect(tmem, tmem + 256 + (i & 7) * 8, bdesc, id, 1u);
+      } else {
+        for (int i = 0; i < iters; ++i) ptx::mma_f16_ss_elect(tmem, adesc, bdesc, id, 1u);
       }
     }
     ptx::tc_commit_elect(&bar);
@@ -78,7 +81,6 @@ __global__ void __launch_bounds__(128, 1) probe(int kind, int ts, int N, int ite
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
-  (void)kind;
 }
 
 int main() {
@@ -90,21 +92,23 @@ int main() {
   const int iters = 4096;
   printf("{\"sm_clock_khz\": %d, \"results\": [\n", clk);
   bool first = true;
+  for (int kind = 0; kind < 2; ++kind)
   for (int ts = 1; ts >= 0; --ts) {
     for (int N : {16, 32, 64, 112, 128, 256}) {
-      probe<<<148, 128, 96 * 1024>>>(0, ts, N, iters, d);
+      probe<<<148, 128, 96 * 1024>>>(kind, ts, N, iters, d);
       cudaError_t e = cudaDeviceSynchronize();
       long long h[148];
       cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
       long long mx = 0;
       for (long long v : h) mx = v > mx ? v : mx;
       const double cyc = static_cast<double>(mx) / iters;
-      // per SM: 128 x N x 8 MACs per tf32 MMA (K = 8)
-      const double macs_per_clk = 128.0 * N * 8 / cyc;
+      // per SM: 128 x N x K MACs per MMA (K = 8 tf32, 16 f16)
+      const double macs_per_clk = 128.0 * N * (kind ? 16 : 8) / cyc;
       const double tflops = 2.0 * macs_per_clk * 148 * clk * 1e3 / 1e12;
-      printf("%s {\"form\": \"%s\", \"kind\": \"tf32\", \"M\": 128, \"N\": %d, \"cycles_per_mma\": %.2f, "
+      printf("%s {\"form\": \"%s\", \"kind\": \"%s\", \"M\": 128, \"N\": %d, \"cycles_per_mma\": %.2f, "
              "\"mac_per_clk_per_sm\": %.1f, \"tflops_at_base_clock\": %.1f, \"err\": \"%s\"}",
-             first ? "" : ",\n", ts ? "TS" : "SS", N, cyc, macs_per_clk, tflops, cudaGetErrorString(e));
+             first ? "" : ",\n", ts ? "TS" : "SS", kind ? "f16" : "tf32", N, cyc, macs_per_clk, tflops,
+             cudaGetErrorString(e));
       first = false;
     }
   }

@@ -23,7 +23,7 @@ NAMES = {1: "g1.enter", 2: "g1.issue", 3: "g2.enter", 4: "g2.issue",
          10: "epi.acc_wait", 11: "epi.acc_got", 12: "epi.computed", 13: "epi.sfree_got", 14: "epi.stored",
          20: "pro.enter", 21: "pro.xfree_got", 22: "pro.done", 23: "rd.ofull_wait", 24: "rd.ofull_got",
          25: "rd.done", 26: "rd.gathered", 30: "prod.dn_wait", 31: "prod.dn_got", 33: "prod.p_got"}
-SLOTS = {0: "producer", 1: "mma", 2: "epi set0", 3: "epi set1"}
+SLOTS = {0: "producer", 1: "mma g1", 2: "epi set0", 3: "epi set1", 4: "mma g2"}
 
 
 def main():
@@ -45,15 +45,15 @@ def main():
     p.estimate_device(g, d_obs, None if "--no-est" in sys.argv else d_est,
                       None if "--no-out" in sys.argv else d_res, st)
     torch.cuda.synchronize()
-    raw = np.fromfile(out, dtype=np.uint64).reshape(4, CAP * 2)
+    raw = np.fromfile(out, dtype=np.uint64).reshape(5, CAP * 2)
     t0 = None
-    for s in range(4):
+    for s in range(5):
         cnt = int(raw[s, 0])
         recs = raw[s, 2:2 + 2 * min(cnt, CAP - 1)].reshape(-1, 2)
         if len(recs) and (t0 is None or recs[0, 1] < t0):
             t0 = int(recs[0, 1])
     total_end = 0
-    for s in range(4):
+    for s in range(5):
         cnt = int(raw[s, 0])
         recs = raw[s, 2:2 + 2 * min(cnt, CAP - 1)].reshape(-1, 2)
         ev = (recs[:, 0] >> 32).astype(int)

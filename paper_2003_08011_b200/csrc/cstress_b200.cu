@@ -289,7 +289,7 @@ bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
 
 // ------------------------------------------------------ FP32 operand packing
 void choose_tc_shape(cs_model* M) {
-  M->K1 = static_cast<int>((M->n + 1 + 15) / 16 * 16);  // + the ||d||^2 column; K = 16 per MMA
+  M->K1 = static_cast<int>((M->n + 2 + 15) / 16 * 16);  // + the ||d||^2, ||x||^2 columns; K = 16 per MMA
   M->N2 = static_cast<int>((M->n + 15) / 16 * 16);
   M->MT = 0;
   // (memory tile MT, TMEM buffers NB) in order of preference.  A TS-form
@@ -610,12 +610,12 @@ PFN_cuTensorMapEncodeTiled_v12000 out_map_encoder() {
 
 // N x n column-major FP32 output (leading dimension ld) as a 2D tensor map
 // whose box is one 128-observation tile of all n signals
-bool encode_out_map(CUtensorMap* m, void* ptr, int64_t N, int n, int64_t ld) {
+bool encode_out_map(CUtensorMap* m, const void* ptr, int64_t N, int n, int64_t ld) {
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(n)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(kObsTile), static_cast<cuuint32_t>(n)};
   const cuuint32_t es[2] = {1, 1};
-  return out_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, es,
+  return out_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

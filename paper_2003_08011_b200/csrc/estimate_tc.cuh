@@ -11,11 +11,12 @@
 //
 // One CTA (persistent, grid = #SMs) owns a 128-observation tile at a time and
 // streams the memory matrix in MT-wide tiles ("steps").  Warp roles:
-//   warp 0       producer: 1D bulk copies (TMA engine) of pre-tiled D_norm^T
-//                and P^T operand tiles into n_stages-deep shared-memory rings
-//   warp 1       MMA issuer (one thread): tcgen05.mma kind::f16.  GEMM1 runs
-//                one or two steps ahead of GEMM2.
-//   warps 2..17  epilogue: two sets of 8 warps; set e owns the steps with
+//   warps 0, 1   producers: 1D bulk copies (TMA engine) of the pre-tiled
+//                D_norm^T (warp 0) and P^T (warp 1) operand tiles into
+//                n_stages-deep shared-memory rings
+//   warps 2, 3   MMA issuers (one thread each): tcgen05.mma kind::f16, GEMM1
+//                (warp 2) one or two steps ahead of GEMM2 (warp 3).
+//   warps 4..19  epilogue: two sets of 8 warps; set e owns the steps with
 //                j % 2 == e (and TMEM buffer e), each warp a 32-lane quarter
 //                and half of the MT columns.  All 16 warps share the x
 //                prologue and the final estimate / residual readout.
@@ -45,7 +46,7 @@ namespace csb {
 
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = 32 * kEpiWarps;         // 512
-constexpr int kTcThreads = 96 + kEpiThreads;        // 608: producer, 2 MMA issuers, epilogue
+constexpr int kTcThreads = 128 + kEpiThreads;       // 640: 2 producers, 2 MMA issuers, epilogue
 constexpr int kObsTile = 128;
 constexpr int kTmemCols = 512;
 constexpr int kMaxStages = 4;
@@ -76,7 +77,7 @@ struct TcParams {
   // staged readout (FP32 I/O when shared memory allows): estimates and
   // residuals of a tile are written to shared memory and leave by two TMA
   // tensor stores (an asynchronous 2 x 51 KB copy at C2 instead of a burst
-  // of 64 scalar stores per thread that stalled every CTA at the tile edge)
+  // of scalar stores per thread that stalled every CTA at the tile edge)
   int staged;
   uint32_t stage_out_off;  // byte offset of the [2][n][128] FP32 staging area
   CUtensorMap tmap_est, tmap_res;
@@ -113,8 +114,25 @@ __host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB, i
 // Shared-memory footprint of everything but the operand rings: barriers,
 // staged scales and the per-row ||x||^2 partials.
 __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
-  return 512 + static_cast<size_t>(K1) * (4 + 4 + 8 + 8) + 4 * kObsTile * 4 + 4 * kObsTile;
+  return 512 + static_cast<size_t>(K1) * (4 + 4 + 8 + 8) + 2 * 4 * kObsTile * 4 + 2 * 4 * kObsTile +
+         2 * kObsTile * 4 + 2 * kObsTile;
 }
+
+// Development switches (A/B builds): how many of every four reciprocals of the
+// inverse-distance map go to MUFU (the rest run as FMA-pipe Newton
+// iterations), and which roles suspend in their mbarrier waits (0 none,
+// 1 epilogue, 2 every role).
+#ifndef CSB_RCP_MUFU
+#define CSB_RCP_MUFU 2
+#endif
+#ifndef CSB_WAIT_SLEEP
+#define CSB_WAIT_SLEEP 1
+#endif
+// 1: with two step sets, the tile-edge prologue and readout run on different
+// sets side by side; 0: all epilogue warps run both in turn
+#ifndef CSB_SPLIT_BOUNDARY
+#define CSB_SPLIT_BOUNDARY 0
+#endif
 
 // ring position: (index, phase) advanced in issue order
 struct Ring {
@@ -139,6 +157,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   static_assert(SB >= 1 && SB <= NB, "S buffers");
   constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
   constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
+  constexpr bool kSplit = CSB_SPLIT_BOUNDARY && NB == 2;  // see CSB_SPLIT_BOUNDARY
   constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
   static_assert(COLS % 8 == 0, "epilogue column slice must be a multiple of 8");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -164,12 +183,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   uint64_t* o_full = bars + 26;
   uint64_t* o_free = bars + 27;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
+  // ||x||^2 hand-off from the prologue set to the readout set (NB = 2):
+  // strictly alternating posted / taken phases, so neither side can lap the
+  // other and parity waits stay unambiguous however short the tile is
+  uint64_t* xx_posted = bars + 29;
+  uint64_t* xx_taken = bars + 30;
   double* s_inv_d = reinterpret_cast<double*>(bars + 64);
   double* s_scale_d = s_inv_d + p.K1;
   float* s_inv_f = reinterpret_cast<float*>(s_scale_d + p.K1);
   float* s_scale_f = s_inv_f + p.K1;
-  float* s_xx = s_scale_f + p.K1;  // [4][kObsTile]
-  uint8_t* s_bad = reinterpret_cast<uint8_t*>(s_xx + 4 * kObsTile);  // [4][kObsTile] out-of-range flags
+  float* s_xx = s_scale_f + p.K1;  // [2][4][kObsTile] ||x||^2 partials (by tile parity)
+  uint8_t* s_bad = reinterpret_cast<uint8_t*>(s_xx + 2 * 4 * kObsTile);  // [2][4][kObsTile] out-of-range flags
+  float* s_xx_tot = reinterpret_cast<float*>(s_bad + 2 * 4 * kObsTile);  // [kObsTile] ||x||^2 per row
+  uint8_t* s_bad_tot = reinterpret_cast<uint8_t*>(s_xx_tot + kObsTile);  // [kObsTile]
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 16; ++i) ptx::mbar_init(&bars[i], 1);
@@ -179,10 +205,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       ptx::mbar_init(&s_ready[b], kSetWarps);
       ptx::mbar_init(&s_free[b], 1);
     }
-    ptx::mbar_init(x_ready, kEpiWarps);
+    ptx::mbar_init(x_ready, kSplit ? kSetWarps : kEpiWarps);
     ptx::mbar_init(x_free, 1);
     ptx::mbar_init(o_full, 1);
-    ptx::mbar_init(o_free, kEpiWarps);
+    ptx::mbar_init(xx_posted, 4);
+    ptx::mbar_init(xx_taken, kSetWarps);
+    ptx::mbar_init(o_free, kSplit ? kSetWarps : kEpiWarps);
     ptx::fence_mbar_init();
   }
   for (int s = threadIdx.x; s < p.K1; s += blockDim.x) {
@@ -204,6 +232,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   if (*tmem_holder != 0u) __trap();
   constexpr uint32_t tmem = 0;
 
+  auto rwait = [](uint64_t* bar, uint32_t parity) {  // producer / MMA waits
+    if constexpr (CSB_WAIT_SLEEP >= 2) {
+      ptx::mbar_wait_sleep(bar, parity);
+    } else {
+      ptx::mbar_wait(bar, parity);
+    }
+  };
   const int K1 = p.K1, N2 = p.N2;
   const uint32_t colO = 0;
   const uint32_t colXh = N2, colXl = N2 + K1 / 2;
@@ -212,10 +247,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   const int n_tiles = static_cast<int>((p.N + kObsTile - 1) / kObsTile);
   const int T = p.m_tiles;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    // (whole warp, converged; one elected lane issues)
+  if (warp <= 1) {
+    // ----------------------------------------------------------- producers
+    // (whole warp, converged; one elected lane issues).  Warp 0 streams the
+    // D_norm^T ring, warp 1 the P^T ring: with one producer for both, the
+    // D tile for GEMM1(j + 1) queued behind the wait for a free P slot, i.e.
+    // behind GEMM2(j - 1) and hence the similarity epilogue, and GEMM1
+    // starved (tools/timeline.py).
     {
+      const bool dn = warp == 0;
+      uint64_t* full = dn ? dn_full : p_full;
+      uint64_t* empty = dn ? dn_empty : p_empty;
+      uint8_t* ring = dn ? dn_ring : p_ring;
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(dn ? static_cast<const void*>(p.dn_tiles)
+                                                               : static_cast<const void*>(p.p_tiles));
+      const uint32_t bytes = dn ? p.dn_stage_bytes : p.p_stage_bytes;
       Ring r(NS);
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         // warm L2 with the next tile's observations (one 128-row segment per
@@ -235,25 +281,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             if (a1 > a0) ptx::prefetch_l2(reinterpret_cast<const void*>(a0), static_cast<uint32_t>(a1 - a0));
           }
         };
-        prefetch_tile(tile + gridDim.x);
+        if (!dn) prefetch_tile(tile + gridDim.x);
         for (int j = 0; j < T; ++j, r.next()) {
-          CSB_TL(0, 30, j);
-          ptx::mbar_wait(&dn_empty[r.idx], r.phase ^ 1);
-          CSB_TL(0, 31, j);
-          ptx::mbar_arrive_expect_tx_elect(&dn_full[r.idx], p.dn_stage_bytes);
-          ptx::bulk_g2s_elect(dn_ring + r.idx * p.dn_stage_bytes,
-                              reinterpret_cast<const uint8_t*>(p.dn_tiles) + static_cast<size_t>(j) * p.dn_stage_bytes,
-                              p.dn_stage_bytes, &dn_full[r.idx]);
-          ptx::mbar_wait(&p_empty[r.idx], r.phase ^ 1);
-          CSB_TL(0, 33, j);
-          ptx::mbar_arrive_expect_tx_elect(&p_full[r.idx], p.p_stage_bytes);
-          ptx::bulk_g2s_elect(p_ring + r.idx * p.p_stage_bytes,
-                              reinterpret_cast<const uint8_t*>(p.p_tiles) + static_cast<size_t>(j) * p.p_stage_bytes,
-                              p.p_stage_bytes, &p_full[r.idx]);
+          if (dn) CSB_TL(0, 30, j);
+          rwait(&empty[r.idx], r.phase ^ 1);
+          if (dn) CSB_TL(0, 31, j);
+          ptx::mbar_arrive_expect_tx_elect(&full[r.idx], bytes);
+          ptx::bulk_g2s_elect(ring + r.idx * bytes, src + static_cast<size_t>(j) * bytes, bytes, &full[r.idx]);
         }
       }
     }
-  } else if (warp == 1 || warp == 2) {
+  } else if (warp == 2 || warp == 3) {
     // ---------------------------------------------------------- MMA issuer
     // (whole warp, converged, warp-uniform operands; one elected lane issues)
     {
@@ -276,9 +314,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       auto issue_g1 = [&](int j) {
         const int b = NB == 2 ? (j & 1) : 0;
         CSB_TL(1, 1, j);
-        if (j == 0) ptx::mbar_wait(x_ready, tcount1 & 1);
-        ptx::mbar_wait(&dn_full[rd.idx], rd.phase);
-        ptx::mbar_wait(&acc_free[b], (acc_use[b] & 1) ^ 1);
+        if (j == 0) rwait(x_ready, tcount1 & 1);
+        rwait(&dn_full[rd.idx], rd.phase);
+        rwait(&acc_free[b], (acc_use[b] & 1) ^ 1);
         ptx::tc_fence_after();
         CSB_TL(1, 2, j);
         const uint32_t dS = tmem + colAcc + b * MT;
@@ -306,9 +344,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       auto issue_g2 = [&](int j) {
         const int b = SB == 2 ? (j & 1) : 0;
         CSB_TL(4, 3, j);
-        ptx::mbar_wait(&s_ready[b], s_use[b] & 1);
-        ptx::mbar_wait(&p_full[rp.idx], rp.phase);
-        if (j == 0) ptx::mbar_wait(o_free, (tcount2 & 1) ^ 1);
+        rwait(&s_ready[b], s_use[b] & 1);
+        rwait(&p_full[rp.idx], rp.phase);
+        if (j == 0) rwait(o_free, (tcount2 & 1) ^ 1);
         ptx::tc_fence_after();
         CSB_TL(4, 4, j);
         const uint64_t bh0 = p_desc0 + rp.idx * p_stage_off;
@@ -339,13 +377,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         rp.next();
       };
 
-      // GEMM1 and GEMM2 are issued by separate warps (1 and 2), each in its
+      // GEMM1 and GEMM2 are issued by separate warps (2 and 3), each in its
       // own step order: GEMM1(j + NB) goes as soon as the epilogue has read
       // ACC(j), whatever S hand-off GEMM2 is waiting on (one issuing warp
       // serialised the two chains; tools/timeline.py).  Every commit tracks
       // only its own warp's MMAs, and all cross-GEMM dependencies are
       // mbarriers (ACC, S, X, O), so the tensor pipe may interleave freely.
-      if (warp == 1) {
+      if (warp == 2) {
         for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
           for (int j = 0; j < T; ++j) issue_g1(j);
       } else {
@@ -355,12 +393,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 3;               // 0..15 (warps 3..18: every lane quarter
+    const int ew = warp - 4;               // 0..15 (warps 4..19: every lane quarter
                                            // appears once in each group of four)
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int set = NB == 2 ? (ew >> 3) : 0;                // step parity owned
     const int half = NB == 2 ? ((ew >> 2) & 1) : (ew >> 2);  // column slice in step
-    const int g4 = ew >> 2;                // 0..3 for prologue / readout split
+    // Tile boundary: with two step sets (NB = 2) the set that does NOT run
+    // the tile's last step stages the next tile's x (prologue) while the set
+    // that does reads O out, so the two run side by side; with one set all 16
+    // warps do both in turn.  Each role is kBW warps = kBG groups of four
+    // (one warp per TMEM lane quarter); gi is this warp's group.
+    constexpr int kBW = kSplit ? kSetWarps : kEpiWarps;
+    constexpr int kBG = kBW / 4;
+    const int last_set = kSplit ? ((T - 1) & 1) : 0;
+    const bool does_readout = !kSplit || set == last_set;
+    const bool does_prologue = !kSplit || set != last_set;
+    const int gi = (ew >> 2) & (kBG - 1);
     const int row = 32 * q + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     const IO* obs = static_cast<const IO*>(p.obs);
@@ -407,33 +455,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       return (valid && s < p.n) ? v : (s == p.n ? p.aug_x : 0.f);
     };
 
+    auto wait = [](uint64_t* bar, uint32_t parity) {
+      if constexpr (CSB_WAIT_SLEEP >= 1) {
+        ptx::mbar_wait_sleep(bar, parity);
+      } else {
+        ptx::mbar_wait(bar, parity);
+      }
+    };
     uint32_t prologue_count = 0;
-    // x prologue: warp group g4 normalises, splits and stores K-chunks
-    // k8 = g4 mod 4 and contributes a partial ||x||^2 for its chunks.  All
+    // x prologue: warp group gi normalises, splits and stores K-chunks
+    // k8 = gi mod kBG and contributes a partial ||x||^2 for its chunks.  All
     // loads of a batch are issued before any is consumed (one HBM latency
-    // per batch instead of one per chunk).
+    // per batch instead of one per chunk).  Column n + 1 of the operand is
+    // ||x||^2 / kXxCol (GEMM1 then yields d2 itself): it is written once the
+    // partials are summed.  Returns ||x||^2 of this thread's row and whether
+    // the row must be recomputed exactly.
     constexpr int PB = sizeof(IO) == 8 ? 2 : 4;  // chunks per load batch
-    auto prologue = [&](int tile) {
+    const uint32_t w_xx = static_cast<uint32_t>(p.n + 1) / 2;  // f16x2 word holding column n + 1
+    auto prologue = [&](int tile, bool& bad_row) -> float {
       CSB_TL(2 + (ew >> 3), 20, tile);
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
       float acc = 0.f;
       bool bad = false;  // a value outside the FP16 split's range: recompute the row exactly
       bool waited = false;
-      for (int k0 = g4; k0 < K1 / 8; k0 += 4 * PB) {
+      const int kt = tile / static_cast<int>(gridDim.x);  // tile index of this CTA
+      for (int k0 = gi; k0 < K1 / 8; k0 += kBG * PB) {
         float xv[PB][8];
         {
           IO raw[PB][8];
 #pragma unroll
           for (int b = 0; b < PB; ++b)
-            if (k0 + 4 * b < K1 / 8) load_chunk(t, valid, min(k0 + 4 * b, (p.n - 1) / 8), raw[b]);
+            if (k0 + kBG * b < K1 / 8) load_chunk(t, valid, min(k0 + kBG * b, (p.n - 1) / 8), raw[b]);
 #pragma unroll
           for (int b = 0; b < PB; ++b)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) xv[b][e] = norm(raw[b][e], (k0 + 4 * b) * 8 + e, valid);
+            for (int e = 0; e < 8; ++e) xv[b][e] = norm(raw[b][e], (k0 + kBG * b) * 8 + e, valid);
         }
         if (!waited) {
-          ptx::mbar_wait(x_free, (prologue_count & 1) ^ 1);
+          wait(x_free, (prologue_count & 1) ^ 1);
           ++prologue_count;
           ptx::tc_fence_after();
           CSB_TL(2 + (ew >> 3), 21, tile);
@@ -441,7 +501,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         }
 #pragma unroll
         for (int b = 0; b < PB; ++b) {
-          const int k8 = k0 + 4 * b;
+          const int k8 = k0 + kBG * b;
           if (k8 >= K1 / 8) break;
           uint32_t hi[4], lo[4];
 #pragma unroll
@@ -458,42 +518,81 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         }
       }
       if (!waited) {
-        ptx::mbar_wait(x_free, (prologue_count & 1) ^ 1);
+        wait(x_free, (prologue_count & 1) ^ 1);
         ++prologue_count;
         ptx::tc_fence_after();
       }
-      s_xx[g4 * kObsTile + row] = acc;
-      s_bad[g4 * kObsTile + row] = bad && valid;
+      const int par = kt & 1;
+      float* xx_part = s_xx + par * 4 * kObsTile;
+      uint8_t* bad_part = s_bad + par * 4 * kObsTile;
+      xx_part[gi * kObsTile + row] = acc;
+      bad_part[gi * kObsTile + row] = bad && valid;
+      ptx::named_bar_sync(1, kBW * 32);
+      float xx = 0.f;
+#pragma unroll
+      for (int g = 0; g < kBG; ++g) {
+        xx += xx_part[g * kObsTile + row];
+        bad |= bad_part[g * kObsTile + row] != 0;
+      }
+      const float xc = xx * (1.f / kXxCol);
+      bad = (bad || !(xc < kF16Safe)) && valid;
+      if (kSplit && gi == 0) {
+        // hand ||x||^2 to the readout set once it has taken the previous one
+        if (kt >= 1) wait(xx_taken, (kt - 1) & 1);
+        s_xx_tot[row] = xx;
+        s_bad_tot[row] = bad;
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(xx_posted);
+      }
+      if (gi == 0) {
+        // the word holding column n + 1 (its partner is the ||d||^2 column n
+        // or the zero column n + 2)
+        const float a = (p.n & 1) ? 0.f : p.aug_x;
+        const float c = bad ? 0.f : xc;
+        uint32_t hi, lo;
+        if (p.n & 1) {
+          ptx::split_f16x2(c, 0.f, hi, lo);
+        } else {
+          ptx::split_f16x2(a, c, hi, lo);
+        }
+        ptx::tmem_st1(tmem + lane_off + colXh + w_xx, hi);
+        ptx::tmem_st1(tmem + lane_off + colXl + w_xx, lo);
+      }
       ptx::tc_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       CSB_TL(2 + (ew >> 3), 22, tile);
       if (lane == 0) ptx::mbar_arrive(x_ready);
-    };
-    bool bad_cur = false;  // row of the current tile recomputed exactly
-    auto gather_xx = [&]() -> float {
-      ptx::named_bar_sync(1, kEpiThreads);
-      float xx = 0.f;
-      bool bad = false;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        xx += s_xx[g * kObsTile + row];
-        bad |= s_bad[g * kObsTile + row] != 0;
-      }
-      ptx::named_bar_sync(1, kEpiThreads);  // partials may be overwritten afterwards
-      bad_cur = bad;
+      bad_row = bad;
       return xx;
     };
-
     uint32_t use = 0, tcount = 0;  // uses of this set's TMEM buffers
     uint32_t s_waits = 0;          // SB = 1, NB = 2: waits on this set's s_free
+    bool bad_cur = false;  // row of the current tile recomputed exactly
     float xx_cur = 0.f, thr_cur = 0.f;
-    auto set_thr = [&]() { thr_cur = p.tau * p.dd_max - (1.f - p.tau) * xx_cur; };
-    if (static_cast<int>(blockIdx.x) < n_tiles) {
-      prologue(blockIdx.x);
-      xx_cur = gather_xx();
+    // every d2 >= thr clears the exact near-zero criterion; thr > 0, so rows
+    // whose minimum passes also need no clamp before the square root
+    auto set_thr = [&]() { thr_cur = p.tau * (xx_cur + p.dd_max); };
+    // TMA store issuer: one fixed thread of the readout role (bulk groups are per thread)
+    const bool issuer_thread = does_readout && ew % kBW == 0 && lane == 0;
+    // ||x||^2 of the row for tile index k (per CTA), staged by the prologue set
+    auto fetch_xx = [&](int k) {
+      wait(xx_posted, k & 1);
+      xx_cur = s_xx_tot[row];
+      bad_cur = s_bad_tot[row] != 0;
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(xx_taken);
       set_thr();
+    };
+    if (static_cast<int>(blockIdx.x) < n_tiles) {
+      if (does_prologue) {
+        xx_cur = prologue(blockIdx.x, bad_cur);
+        set_thr();
+      } else {
+        fetch_xx(0);
+      }
     }
+    const float inv_h_s = p.inv_h * (1.f / kSScale);  // exact power-of-two rescaling
     const uint32_t a_base = colAcc + set * MT + c0;
     const int sbuf = SB == 2 ? set : 0;
     const uint32_t s_base = colS + sbuf * MT + c0 / 2;  // f16x2: two columns per word
@@ -517,15 +616,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           ptx::tc_wait_ld();
         };
         auto compute_chunk = [&](int c, float* v) {
-          // ACC = ||d||^2 - 2 x.d (tensor core); d2 = ACC + ||x||^2.  The
-          // prefilter min(ACC) < thr is a superset of the exact near-zero
-          // criterion d2 < tau (||x||^2 + ||d||^2), re-checked per entry.
+          // ACC = d2 = ||x||^2 + ||d||^2 - 2 x.d (tensor core).  The
+          // prefilter min(d2) < tau (||x||^2 + max ||d||^2) is a superset of
+          // the exact near-zero criterion d2 < tau (||x||^2 + ||d||^2),
+          // re-checked per entry; recomputed entries are >= 0, all others
+          // >= the criterion's bound >= 0.
           float mn = v[0];
 #pragma unroll
-          for (int e = 0; e < CH; ++e) {
-            mn = fminf(mn, v[e]);
-            v[e] += xx_cur;
-          }
+          for (int e = 1; e < CH; ++e) mn = fminf(mn, v[e]);
           if ((mn < thr_cur || bad_cur) && valid) {  // rare: direct difference, not unrolled
 #pragma unroll 1
             for (int e = 0; e < CH; ++e) {
@@ -546,17 +644,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
                 if (ee == e) v[ee] = a;
             }
           }
+          // S scaled by 2^14 (FP16 split range, pack_tc.cuh)
           if (gaussian) {
 #pragma unroll
-            for (int e = 0; e < CH; ++e) v[e] = ptx::ex2_approx(-fmaxf(v[e], 0.f) * p.g_coef);
+            for (int e = 0; e < CH; ++e) v[e] = ptx::ex2_approx(-v[e] * p.g_coef) * kSScale;
           } else {
-            // 1 / (1 + sqrt(d2)/h): sqrt on the MUFU pipe; the reciprocal
-            // alternates between MUFU and an FMA-pipe Newton iteration so the
-            // two pipes share the work.
+            // 2^14 / (1 + sqrt(d2)/h) = 1 / (2^-14 + sqrt(d2) (2^-14/h)): the
+            // scale folds into the FMA exactly.  sqrt on the MUFU pipe; of
+            // every four reciprocals CSB_RCP_MUFU go to MUFU, the rest to an
+            // FMA-pipe Newton iteration, so the two pipes share the work.
 #pragma unroll
             for (int e = 0; e < CH; ++e) {
-              const float x = fmaf(ptx::sqrt_approx(fmaxf(v[e], 0.f)), p.inv_h, 1.f);
-              v[e] = (e & 1) ? ptx::rcp_newton(x) : ptx::rcp_approx(x);
+              const float x = fmaf(ptx::sqrt_approx(v[e]), inv_h_s, 1.f / kSScale);
+              v[e] = (e & 3) < CSB_RCP_MUFU ? ptx::rcp_approx(x) : ptx::rcp_newton(x);
             }
           }
           if (valid_cols < (c + 1) * CH) {
@@ -572,13 +672,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             uint32_t hi[4], lo[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              ptx::split_f16x2(v[h8 * 8 + 2 * e] * kSScale, v[h8 * 8 + 2 * e + 1] * kSScale, hi[e], lo[e]);
+              ptx::split_f16x2(v[h8 * 8 + 2 * e], v[h8 * 8 + 2 * e + 1], hi[e], lo[e]);
             ptx::tmem_st4(tmem + lane_off + s_base + (c * CH + h8 * 8) / 2, hi);
             ptx::tmem_st4(tmem + lane_off + s_base + MT / 2 + (c * CH + h8 * 8) / 2, lo);
           }
         };
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 10, j);
-        ptx::mbar_wait(&acc_full[set], use & 1);
+        wait(&acc_full[set], use & 1);
         ptx::tc_fence_after();
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 11, j);
         if constexpr (SB == 1) {
@@ -598,9 +698,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
           if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
           if constexpr (NB == 1) {
-            ptx::mbar_wait(&s_free[0], (use & 1) ^ 1);
+            wait(&s_free[0], (use & 1) ^ 1);
           } else if (tcount != 0 || j != 0) {  // the CTA's first step has no predecessor
-            ptx::mbar_wait(&s_free[set], s_waits & 1);
+            wait(&s_free[set], s_waits & 1);
             ++s_waits;
           }
           ptx::tc_fence_after();
@@ -615,13 +715,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
-          ptx::mbar_wait(&s_free[set], (use & 1) ^ 1);
-          ptx::tc_fence_after();
+          // map first, then wait for GEMM2(j - 2) to have read S[set]
 #pragma unroll
-          for (int c = 0; c < COLS / CH; ++c) {
-            compute_chunk(c, vall + c * CH);
-            store_chunk(c, vall + c * CH);
-          }
+          for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
+          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
+          wait(&s_free[set], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 13, j);
+#pragma unroll
+          for (int c = 0; c < COLS / CH; ++c) store_chunk(c, vall + c * CH);
         }
         ptx::tc_wait_st();
         ptx::tc_fence_before();
@@ -631,90 +733,98 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       }
       // next tile's x prologue overlaps this tile's last GEMM2
       const int next = tile + gridDim.x;
-      if (next < n_tiles) prologue(next);
+      float xx_next = 0.f;
+      bool bad_next = false;
+      if (does_prologue && next < n_tiles) xx_next = prologue(next, bad_next);
 
       // readout: estimate = scale .* O, residual = x - estimate.  The raw
       // observations of a batch are loaded before waiting for O.
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
-      float* s_out = reinterpret_cast<float*>(smem + p.stage_out_off);  // [2][n][128]
-      const bool issuer = ew == 0 && lane == 0;                         // TMA store issuer
-      if (p.staged) {
-        // the previous tile's TMA stores must have read the staging area
-        if (issuer) ptx::bulk_wait_read0();
-        ptx::named_bar_sync(2, kEpiThreads);
-      }
-      bool o_ready = false;
-      for (int cb = g4; cb < N2 / 8; cb += 4 * PB) {
-        IO xr[PB][8];
-#pragma unroll
-        for (int b = 0; b < PB; ++b)
-          if (cb + 4 * b < N2 / 8) load_chunk(t, valid, min(cb + 4 * b, (p.n - 1) / 8), xr[b]);
-        if (!o_ready) {
-          ptx::mbar_wait(o_full, tcount & 1);
-          ptx::tc_fence_after();
-          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
-          o_ready = true;
+      const bool issuer = issuer_thread;
+      if (does_readout) {
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
+        float* s_out = reinterpret_cast<float*>(smem + p.stage_out_off);  // [2][n][128]
+        if (p.staged) {
+          // the previous tile's TMA stores must have read the staging area
+          if (issuer) ptx::bulk_wait_read0();
+          ptx::named_bar_sync(2, kBW * 32);
         }
+        // x loads of all of a thread's chunks are issued before O is waited
+        // for (one latency); O is read a chunk at a time (register pressure)
+        constexpr int RB = kBG == 4 ? PB : 2;
+        bool o_ready = false;
+        for (int cb = gi; cb < N2 / 8; cb += kBG * RB) {
+          IO xr[RB][8];
 #pragma unroll
-        for (int b = 0; b < PB; ++b) {
-          const int c = cb + 4 * b;
-          if (c >= N2 / 8) break;
-          float o[8];
-          ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+          for (int b = 0; b < RB; ++b)
+            if (cb + kBG * b < N2 / 8) load_chunk(t, valid, min(cb + kBG * b, (p.n - 1) / 8), xr[b]);
+          if (!o_ready) {
+            wait(o_full, tcount & 1);
+            ptx::tc_fence_after();
+            if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
+            o_ready = true;
+          }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int s = c * 8 + e;
-            const bool ok = valid && s < p.n;
-            const int64_t idx = t + static_cast<int64_t>(s) * p.ld;
-            if constexpr (sizeof(IO) == 8) {
-              const double ev = static_cast<double>(o[e]) * s_scale_d[s];
-              if (ok && est) est[idx] = ev;
-              if (ok && resid) resid[idx] = xr[b][e] - ev;
-            } else {
-              const float ev = o[e] * s_scale_f[s];
-              if (p.staged) {
-                if (s < p.n) {
-                  s_out[s * kObsTile + row] = ev;
-                  s_out[(p.n + s) * kObsTile + row] = xr[b][e] - ev;
-                }
-              } else {
+          for (int b = 0; b < RB; ++b) {
+            const int c = cb + kBG * b;
+            if (c >= N2 / 8) break;
+            float o[8];
+            ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int s = c * 8 + e;
+              const bool ok = valid && s < p.n;
+              const int64_t idx = t + static_cast<int64_t>(s) * p.ld;
+              if constexpr (sizeof(IO) == 8) {
+                const double ev = static_cast<double>(o[e]) * s_scale_d[s];
                 if (ok && est) est[idx] = ev;
                 if (ok && resid) resid[idx] = xr[b][e] - ev;
+              } else {
+                const float ev = o[e] * s_scale_f[s];
+                if (p.staged) {
+                  if (s < p.n) {
+                    s_out[s * kObsTile + row] = ev;
+                    s_out[(p.n + s) * kObsTile + row] = xr[b][e] - ev;
+                  }
+                } else {
+                  if (ok && est) est[idx] = ev;
+                  if (ok && resid) resid[idx] = xr[b][e] - ev;
+                }
               }
             }
           }
         }
-      }
-      if (!o_ready) {
-        ptx::mbar_wait(o_full, tcount & 1);
-        ptx::tc_fence_after();
-      }
-      if (p.staged) {
+        if (!o_ready) {
+          wait(o_full, tcount & 1);
+          ptx::tc_fence_after();
+        }
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 27, tile);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(o_free);  // O read: the next tile's GEMM2 may start
-        ptx::fence_proxy_async_smem();
-        ptx::named_bar_sync(2, kEpiThreads);
-        if (issuer) {
-          const int t0 = tile * kObsTile;
-          if (est) ptx::tma_store_2d(&p.tmap_est, t0, 0, s_out);
-          if (resid) ptx::tma_store_2d(&p.tmap_res, t0, 0, s_out + p.n * kObsTile);
-          ptx::bulk_commit();
+        if (p.staged) {
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(2, kBW * 32);
+          if (issuer) {
+            const int t0 = tile * kObsTile;
+            if (est) ptx::tma_store_2d(&p.tmap_est, t0, 0, s_out);
+            if (resid) ptx::tma_store_2d(&p.tmap_res, t0, 0, s_out + p.n * kObsTile);
+            ptx::bulk_commit();
+          }
         }
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
       }
-      if (!p.staged) {
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(o_free);
-      }
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
       if (next < n_tiles) {
-        xx_cur = gather_xx();
-        set_thr();
+        if (does_prologue) {
+          xx_cur = xx_next;
+          bad_cur = bad_next;
+          set_thr();
+        } else {
+          fetch_xx(tcount + 1);
+        }
       }
       if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 26, tile);
     }
-    if (p.staged && ew == 0 && lane == 0) ptx::bulk_wait0();  // stores complete before exit
+    if (p.staged && issuer_thread) ptx::bulk_wait0();  // stores complete before exit
   }
   __syncthreads();
   if (warp == 0) {

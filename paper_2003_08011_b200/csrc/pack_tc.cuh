@@ -21,6 +21,10 @@ namespace csb {
 
 constexpr float kSScale = 16384.f;  // 2^14: S in (0, 1] -> normal FP16 range
 constexpr float kF16Safe = 32768.f;  // |operand| >= this is outside the split's safe range
+// Fused kernel: D_norm^T tiles carry this constant in column n + 1 and the
+// observation operand carries ||x||^2 / kXxCol there, so GEMM1 accumulates
+// the whole d2 = ||x||^2 + ||d||^2 - 2 x.d (power of two: exact)
+constexpr float kXxCol = 16.f;
 
 // Canonical K-major, no-swizzle layout of an R x K block of 16-bit
 // elements: core matrices of 8 rows x 16 bytes; element (r, k) at
@@ -36,8 +40,9 @@ __device__ __forceinline__ void split_f16(double v, __half& hi, __half& lo) {
 
 // D_norm^T tiles: block j holds memory vectors j*MT.. as rows, signals as K:
 // column k < n holds -2 d_k (exact), column n holds ||d||^2 * aug_scale
-// (FP64, split) -- with x augmented by 1/aug_scale in column n, GEMM1 yields
-// ||d||^2 - 2 x.d directly (one FADD of ||x||^2 left).
+// (FP64, split), column n + 1 the constant kXxCol -- with x augmented by
+// 1/aug_scale in column n and ||x||^2 / kXxCol in column n + 1, GEMM1 yields
+// d2 = ||x||^2 + ||d||^2 - 2 x.d directly.
 __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m, int MT, int K1,
                                      int m_tiles, double aug_scale, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(MT) * K1;
@@ -58,6 +63,8 @@ __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m
           v = fma(d, d, v);
         }
         v *= aug_scale;
+      } else if (k == n + 1) {
+        v = kXxCol;
       }
     }
     __half hi, lo;

@@ -8,7 +8,7 @@ bit-exactness claims of this build:
   * select_memory_vectors: bitwise equal indices;
   * FP64 estimate given the same model: bitwise equal to the reference
     association and order;
-  * FP32 (tcgen05 3xTF32) estimate: max|est - est_ref| <= 1e-3 max|est_ref|
+  * FP32 (tcgen05 3xFP16) estimate: max|est - est_ref| <= 1e-3 max|est_ref|
     (north_star tolerance; typical 1e-6..1e-5).
 """
 import numpy as np
@@ -398,3 +398,32 @@ def test_staged_readout_matches_direct_stores(p, oracle, n, m, N):
     assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
     want = p.estimate(g, obs).estimates
     assert rel(out["1"][0].astype(np.float64), want) <= 1e-5
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("shape", ["64,2,2", "64,2,1", "64,1,1", "32,2,2", "128,1,1"])
+@pytest.mark.parametrize("n,m", [(20, 64), (20, 100), (24, 150), (100, 1000)])
+def test_fused_many_tiles_per_cta(p, oracle, shape, n, m):
+    """Fused kernel with several observation tiles per CTA (148 persistent
+    CTAs, >= 3 tiles each) for every (MT, NB, SB) TMEM plan and 1..16 memory
+    tiles per observation tile: the tile-boundary hand-offs (x prologue,
+    ||x||^2 hand-over, O readout) must neither deadlock nor mix tiles.
+    Checked against the GPU FP64 estimate (bitwise the reference order) of
+    the same training data, and a sample against the oracle."""
+    import os
+    N = 148 * 128 * 3 + 77
+    X = oracle.synthesize_uniform(n, 4 * m, 0.5, 0.3, 1.0, 0.5, 4.0, 31 + n)
+    obs = oracle.synthesize_uniform(n, N, 0.5, 0.3, 1.0, 0.5, 4.0, 37 + n)
+    os.environ["CSB_TC_SHAPE"] = shape
+    try:
+        g = p.train(X, m, p.KernelConfig(), B(p, "fp32"))
+    finally:
+        del os.environ["CSB_TC_SHAPE"]
+    g64 = p.train(X, m, p.KernelConfig(), B(p, "fp64"))
+    want = p.estimate(g64, obs).estimates
+    r = p.estimate(g, obs)
+    assert rel(r.estimates, want) <= FP32_TOL
+    assert np.array_equal(r.residuals, obs - r.estimates)
+    sel = np.arange(0, N, 997)
+    o = oracle.train(X, m, 0)
+    assert rel(r.estimates[sel], oracle.estimate(o, obs[sel])[0]) <= FP32_TOL

@@ -22,7 +22,7 @@ CAP = 8192
 NAMES = {1: "g1.enter", 2: "g1.issue", 3: "g2.enter", 4: "g2.issue",
          10: "epi.acc_wait", 11: "epi.acc_got", 12: "epi.computed", 13: "epi.sfree_got", 14: "epi.stored",
          20: "pro.enter", 21: "pro.xfree_got", 22: "pro.done", 23: "rd.ofull_wait", 24: "rd.ofull_got",
-         25: "rd.done", 26: "rd.gathered", 30: "prod.dn_wait", 31: "prod.dn_got", 33: "prod.p_got"}
+         25: "rd.done", 26: "rd.gathered", 27: "rd.looped", 30: "prod.dn_wait", 31: "prod.dn_got", 33: "prod.p_got"}
 SLOTS = {0: "producer", 1: "mma g1", 2: "epi set0", 3: "epi set1", 4: "mma g2"}
 
 
@@ -74,6 +74,21 @@ def main():
         if "--raw" in sys.argv:
             print("\n".join(lines))
     print(f"kernel span (CTA 0, first->last event): {total_end} cycles")
+    if "--merged" in sys.argv:
+        # all roles interleaved in time over a window of the run
+        allev = []
+        for s in range(5):
+            cnt = int(raw[s, 0])
+            recs = raw[s, 2:2 + 2 * min(cnt, CAP - 1)].reshape(-1, 2)
+            for e, c in recs:
+                allev.append((int(c) - t0, SLOTS[s], NAMES.get(int(e) >> 32, int(e) >> 32), int(e) & 0xFFFFFFFF))
+        allev.sort()
+        lo, hi = total_end // 3, total_end // 3 + 60000
+        prev = None
+        for c, who, what, j in allev:
+            if lo <= c <= hi:
+                print(f"{c:9d} {'' if prev is None else f'+{c - prev:6d}'} {who:9s} {what}({j})")
+                prev = c
 
 
 if __name__ == "__main__":

@@ -17,7 +17,10 @@
 #include <string>
 #include <vector>
 #include <chrono>
+#include <map>
 #include <mutex>
+#include <tuple>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -653,16 +656,17 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   p.p_stage_bytes = static_cast<uint32_t>(2 * M->N2 * M->MT * 2);
   p.n_stages = M->n_stages;
   size_t smem = M->n_stages * (static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes) + tc_aux_bytes(p.K1);
-  // staged readout: FP32 I/O, TMA-compatible outputs (16-byte aligned,
-  // leading dimension a multiple of 4) and room for [2][n][128] FP32 next to
-  // an operand ring of >= 2 stages
+  // staged tile edge: FP32 I/O, TMA-compatible input and outputs (16-byte
+  // aligned, leading dimension a multiple of 4) and room for [2][n][128]
+  // FP32 next to an operand ring of >= 2 stages
   p.staged = 0;
   if constexpr (sizeof(IO) == 4) {
     const size_t stage = static_cast<size_t>(p.dn_stage_bytes) + p.p_stage_bytes;
     const size_t out_bytes = static_cast<size_t>(2) * M->n * kObsTile * 4;
     const size_t budget = 227 * 1024;
     const bool aligned = (ld % 4 == 0) && (reinterpret_cast<uintptr_t>(est) % 16 == 0) &&
-                         (reinterpret_cast<uintptr_t>(resid) % 16 == 0) && (est || resid);
+                         (reinterpret_cast<uintptr_t>(resid) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(obs) % 16 == 0) && (est || resid);
     const char* env = std::getenv("CSB_STAGED_READOUT");
     const bool allow = !(env && env[0] == '0');
     if (allow && aligned && M->n <= 256 && tc_aux_bytes(p.K1) + out_bytes + 128 + 2 * stage <= budget &&
@@ -672,7 +676,7 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
       p.n_stages = ns;
       p.stage_out_off = static_cast<uint32_t>((ns * stage + tc_aux_bytes(p.K1) + 127) / 128 * 128);
       smem = p.stage_out_off + out_bytes;
-      bool ok = true;
+      bool ok = encode_out_map(&p.tmap_obs, obs, N, static_cast<int>(M->n), ld);
       if (est) ok = ok && encode_out_map(&p.tmap_est, est, N, static_cast<int>(M->n), ld);
       if (resid) ok = ok && encode_out_map(&p.tmap_res, resid, N, static_cast<int>(M->n), ld);
       if (ok) {
@@ -693,7 +697,60 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
   auto go = [&](auto kernel) {
     CSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    kernel<<<grid, kTcThreads, smem, st>>>(p);
+    // CSB_CLUSTER=2|4: clusters of CTAs share the operand stream by multicast
+    // (estimate_tc.cuh); the persistent grid is sized to the clusters that
+    // fit at once.  Off by default: measured no faster at C2 (the operand
+    // stream from L2 is not what bounds the step).
+    int cl = 1;
+    if (const char* e = std::getenv("CSB_CLUSTER")) cl = std::max(1, std::atoi(e));
+    int g = grid;
+    if (cl > 1) {
+      static std::mutex mu;
+      static std::map<std::tuple<const void*, size_t, int>, int> fit;  // max active clusters
+      std::lock_guard<std::mutex> lock(mu);
+      const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), smem, cl);
+      auto it = fit.find(key);
+      if (it == fit.end()) {
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(static_cast<unsigned>(ctx->sm_count / cl * cl));
+        q.blockDim = dim3(kTcThreads);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute a{};
+        a.id = cudaLaunchAttributeClusterDimension;
+        a.val.clusterDim.x = cl;
+        a.val.clusterDim.y = 1;
+        a.val.clusterDim.z = 1;
+        q.attrs = &a;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kernel, &q) != cudaSuccess) {
+          cudaGetLastError();
+          n = 0;
+        }
+        it = fit.emplace(key, n).first;
+      }
+      const int max_ctas = it->second * cl;
+      g = (grid + cl - 1) / cl * cl;
+      if (max_ctas < cl) {
+        cl = 1;
+        g = grid;
+      } else if (g > max_ctas) {
+        g = max_ctas;
+      }
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(g));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cl;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = cl > 1 ? 1 : 0;
+    CSB_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
     CSB_LAUNCH_CHECK();
 #ifdef CSB_TIMELINE
     std::vector<unsigned long long> h(static_cast<size_t>(5) * kTlCap * 2);
@@ -707,19 +764,30 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
     }
 #endif
   };
-  switch (M->MT * 100 + M->NB * 10 + M->SB) {
-    case 12822: go(mset_estimate_tc_kernel<128, 2, 2, IO>); break;
-    case 6422: go(mset_estimate_tc_kernel<64, 2, 2, IO>); break;
-    case 6421: go(mset_estimate_tc_kernel<64, 2, 1, IO>); break;
-    case 4821: go(mset_estimate_tc_kernel<48, 2, 1, IO>); break;
-    case 12811: go(mset_estimate_tc_kernel<128, 1, 1, IO>); break;
-    case 6411: go(mset_estimate_tc_kernel<64, 1, 1, IO>); break;
-    case 3222: go(mset_estimate_tc_kernel<32, 2, 2, IO>); break;
-    case 3221: go(mset_estimate_tc_kernel<32, 2, 1, IO>); break;
-    case 3211: go(mset_estimate_tc_kernel<32, 1, 1, IO>); break;
-    case 1622: go(mset_estimate_tc_kernel<16, 2, 2, IO>); break;
-    default: fail(CS_ERROR, "internal: bad tensor-core tile shape");
+  // staged tile edge (FP32 I/O) and plain variants of each TMEM plan
+  auto pick = [&](auto staged_tag) {
+    constexpr bool S = decltype(staged_tag)::value;
+    switch (M->MT * 100 + M->NB * 10 + M->SB) {
+      case 12822: go(mset_estimate_tc_kernel<128, 2, 2, IO, S>); return true;
+      case 6422: go(mset_estimate_tc_kernel<64, 2, 2, IO, S>); return true;
+      case 6421: go(mset_estimate_tc_kernel<64, 2, 1, IO, S>); return true;
+      case 4821: go(mset_estimate_tc_kernel<48, 2, 1, IO, S>); return true;
+      case 12811: go(mset_estimate_tc_kernel<128, 1, 1, IO, S>); return true;
+      case 6411: go(mset_estimate_tc_kernel<64, 1, 1, IO, S>); return true;
+      case 3222: go(mset_estimate_tc_kernel<32, 2, 2, IO, S>); return true;
+      case 3221: go(mset_estimate_tc_kernel<32, 2, 1, IO, S>); return true;
+      case 3211: go(mset_estimate_tc_kernel<32, 1, 1, IO, S>); return true;
+      case 1622: go(mset_estimate_tc_kernel<16, 2, 2, IO, S>); return true;
+    }
+    return false;
+  };
+  bool launched;
+  if constexpr (sizeof(IO) == 4) {
+    launched = p.staged ? pick(std::true_type{}) : pick(std::false_type{});
+  } else {
+    launched = pick(std::false_type{});
   }
+  if (!launched) fail(CS_ERROR, "internal: bad tensor-core tile shape");
 }
 
 // Large-n surveillance: per observation block, pack x -> GEMM-A (similarity

@@ -74,13 +74,17 @@ struct TcParams {
   void* resid;
   uint32_t dn_stage_bytes, p_stage_bytes;
   unsigned long long* timeline;  // CSB_TIMELINE builds only: per-warp event records
-  // staged readout (FP32 I/O when shared memory allows): estimates and
-  // residuals of a tile are written to shared memory and leave by two TMA
-  // tensor stores (an asynchronous 2 x 51 KB copy at C2 instead of a burst
-  // of scalar stores per thread that stalled every CTA at the tile edge)
+  // staged tile edge (FP32 I/O when shared memory allows): a [2][n][128]
+  // FP32 staging area, halves A and B.  During tile k TMA loads x(k + 1)
+  // into A (for the next prologue) and x(k) into B (for this readout); at
+  // the edge the prologue reads A, the readout reads B, writes the residuals
+  // over B and the estimates over A, and two TMA tensor stores write them
+  // back asynchronously.  No global loads or stores at the tile edge: with
+  // per-thread loads the x prologue and readout each waited ~6k cycles on
+  // spilled load batches.
   int staged;
-  uint32_t stage_out_off;  // byte offset of the [2][n][128] FP32 staging area
-  CUtensorMap tmap_est, tmap_res;
+  uint32_t stage_out_off;  // byte offset of the staging area
+  CUtensorMap tmap_obs, tmap_est, tmap_res;
 };
 
 // Development instrumentation (tools/timeline.py): with -DCSB_TIMELINE the
@@ -88,15 +92,16 @@ struct TcParams {
 // triples; compiled out otherwise.
 #ifdef CSB_TIMELINE
 constexpr int kTlCap = 8192;
+// one recording thread per slot keeps its record count in a register (tl_n):
+// a counter in global memory cost a dependent L2 round trip per event and
+// distorted the short phases being measured
 #define CSB_TL(slot, ev, j)                                                                   \
   do {                                                                                      \
-    if (blockIdx.x == 0 && lane == 0 && p.timeline) {                                       \
+    if (blockIdx.x == 0 && lane == 0 && p.timeline && tl_n + 1 < kTlCap) {                  \
       unsigned long long* tl_ = p.timeline + (slot) * kTlCap * 2;                             \
-      const unsigned long long k_ = tl_[0]++;                                               \
-      if (k_ + 1 < kTlCap) {                                                                \
-        tl_[2 + 2 * k_] = (static_cast<unsigned long long>(ev) << 32) | static_cast<unsigned>(j); \
-        tl_[3 + 2 * k_] = clock64();                                                        \
-      }                                                                                     \
+      tl_[2 + 2 * tl_n] = (static_cast<unsigned long long>(ev) << 32) | static_cast<unsigned>(j); \
+      tl_[3 + 2 * tl_n] = clock64();                                                        \
+      tl_[0] = ++tl_n;                                                                      \
     }                                                                                       \
   } while (0)
 #else
@@ -121,17 +126,13 @@ __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
 // Development switches (A/B builds): how many of every four reciprocals of the
 // inverse-distance map go to MUFU (the rest run as FMA-pipe Newton
 // iterations), and which roles suspend in their mbarrier waits (0 none,
-// 1 epilogue, 2 every role).
+// 1 epilogue, 2 every role; measured: 0 is as fast at C2 and 9% faster at
+// n = 20).
 #ifndef CSB_RCP_MUFU
 #define CSB_RCP_MUFU 2
 #endif
 #ifndef CSB_WAIT_SLEEP
-#define CSB_WAIT_SLEEP 1
-#endif
-// 1: with two step sets, the tile-edge prologue and readout run on different
-// sets side by side; 0: all epilogue warps run both in turn
-#ifndef CSB_SPLIT_BOUNDARY
-#define CSB_SPLIT_BOUNDARY 0
+#define CSB_WAIT_SLEEP 0
 #endif
 
 // ring position: (index, phase) advanced in issue order
@@ -151,13 +152,13 @@ struct Ring {
 //         buffer between the sets (GEMM1 still never waits for the
 //         similarity epilogue).  NB = 1: single buffers, all 16 epilogue
 //         warps work on every step (4 column groups), GEMM1 one step ahead.
-template <int MT, int NB, int SB, typename IO>
+template <int MT, int NB, int SB, typename IO, bool STAGED>
 __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const __grid_constant__ TcParams p) {
   static_assert(NB == 1 || NB == 2, "one or two TMEM buffers");
   static_assert(SB >= 1 && SB <= NB, "S buffers");
+  static_assert(!STAGED || sizeof(IO) == 4, "staged tile edge: FP32 I/O");
   constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
   constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
-  constexpr bool kSplit = CSB_SPLIT_BOUNDARY && NB == 2;  // see CSB_SPLIT_BOUNDARY
   constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
   static_assert(COLS % 8 == 0, "epilogue column slice must be a multiple of 8");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -166,6 +167,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / 32, 0);
   const int lane = threadIdx.x % 32;
   const int NS = p.n_stages;
+#ifdef CSB_TIMELINE
+  int tl_n = 0;  // timeline records written by this thread
+#endif
   constexpr int io_bytes = sizeof(IO);
   uint8_t* dn_ring = smem;
   uint8_t* p_ring = smem + NS * p.dn_stage_bytes;
@@ -183,34 +187,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   uint64_t* o_full = bars + 26;
   uint64_t* o_free = bars + 27;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
-  // ||x||^2 hand-off from the prologue set to the readout set (NB = 2):
-  // strictly alternating posted / taken phases, so neither side can lap the
-  // other and parity waits stay unambiguous however short the tile is
-  uint64_t* xx_posted = bars + 29;
-  uint64_t* xx_taken = bars + 30;
+  uint64_t* xa_full = bars + 29;  // staged: x of the next tile in staging half A
+  uint64_t* xb_full = bars + 30;  // staged: x of this tile in staging half B
   double* s_inv_d = reinterpret_cast<double*>(bars + 64);
   double* s_scale_d = s_inv_d + p.K1;
   float* s_inv_f = reinterpret_cast<float*>(s_scale_d + p.K1);
   float* s_scale_f = s_inv_f + p.K1;
   float* s_xx = s_scale_f + p.K1;  // [2][4][kObsTile] ||x||^2 partials (by tile parity)
   uint8_t* s_bad = reinterpret_cast<uint8_t*>(s_xx + 2 * 4 * kObsTile);  // [2][4][kObsTile] out-of-range flags
-  float* s_xx_tot = reinterpret_cast<float*>(s_bad + 2 * 4 * kObsTile);  // [kObsTile] ||x||^2 per row
-  uint8_t* s_bad_tot = reinterpret_cast<uint8_t*>(s_xx_tot + kObsTile);  // [kObsTile]
 
+  // Thread-block cluster of CL CTAs (CL = 1 without a cluster launch): the
+  // operand tiles are identical for every CTA, so each CTA's producer copies
+  // a 1/CL slice of each stage and multicasts it into every CTA of the
+  // cluster (L2 -> SM operand traffic / CL: with one copy per CTA the 148
+  // SMs streaming the same tiles out of L2 bounded the step time); a ring
+  // slot is refilled once the MMAs of every CTA have released it.
+  const uint32_t CL = ptx::cluster_nctarank();
+  const uint32_t cl_rank = CL > 1 ? ptx::cluster_ctarank() : 0;
+  const uint16_t cl_mask = static_cast<uint16_t>((1u << CL) - 1);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 16; ++i) ptx::mbar_init(&bars[i], 1);
+    for (int i = 0; i < 16; ++i) ptx::mbar_init(&bars[i], (i & 4) ? CL : 1);  // [4..7], [12..15]: empty
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&acc_full[b], 1);
       ptx::mbar_init(&acc_free[b], kSetWarps);
       ptx::mbar_init(&s_ready[b], kSetWarps);
       ptx::mbar_init(&s_free[b], 1);
     }
-    ptx::mbar_init(x_ready, kSplit ? kSetWarps : kEpiWarps);
+    ptx::mbar_init(x_ready, kEpiWarps);
     ptx::mbar_init(x_free, 1);
     ptx::mbar_init(o_full, 1);
-    ptx::mbar_init(xx_posted, 4);
-    ptx::mbar_init(xx_taken, kSetWarps);
-    ptx::mbar_init(o_free, kSplit ? kSetWarps : kEpiWarps);
+    ptx::mbar_init(xa_full, 1);
+    ptx::mbar_init(xb_full, 1);
+    ptx::mbar_init(o_free, kEpiWarps);
     ptx::fence_mbar_init();
   }
   for (int s = threadIdx.x; s < p.K1; s += blockDim.x) {
@@ -231,6 +239,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   // tcgen05.mma into an R2UR/VOTEU waterfall.
   if (*tmem_holder != 0u) __trap();
   constexpr uint32_t tmem = 0;
+  if (CL > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast
 
   auto rwait = [](uint64_t* bar, uint32_t parity) {  // producer / MMA waits
     if constexpr (CSB_WAIT_SLEEP >= 2) {
@@ -246,6 +255,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   const uint32_t colS = colAcc + NB * MT;  // + b*MT (hi), + MT/2 (lo)
   const int n_tiles = static_cast<int>((p.N + kObsTile - 1) / kObsTile);
   const int T = p.m_tiles;
+  // tile slots: every CTA of a cluster runs as many as the cluster's first
+  // CTA (the operand rings are shared); slots past the last tile are dummies
+  // with no valid rows.  Slot k of this CTA is tile blockIdx.x + k * grid.
+  const int cl_base = static_cast<int>(blockIdx.x - cl_rank);
+  const int n_iter = cl_base < n_tiles ? (n_tiles - cl_base + static_cast<int>(gridDim.x) - 1) / gridDim.x : 0;
+  const int tile_end = static_cast<int>(blockIdx.x) + n_iter * static_cast<int>(gridDim.x);  // loop bound
 
   if (warp <= 1) {
     // ----------------------------------------------------------- producers
@@ -263,7 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
                                                                : static_cast<const void*>(p.p_tiles));
       const uint32_t bytes = dn ? p.dn_stage_bytes : p.p_stage_bytes;
       Ring r(NS);
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int tile = blockIdx.x; tile < tile_end; tile += gridDim.x) {
         // warm L2 with the next tile's observations (one 128-row segment per
         // signal column): the x prologue then reads L2, not a DRAM burst
         // that every CTA issues at the same moment.  Issued at the start of
@@ -281,13 +296,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             if (a1 > a0) ptx::prefetch_l2(reinterpret_cast<const void*>(a0), static_cast<uint32_t>(a1 - a0));
           }
         };
-        if (!dn) prefetch_tile(tile + gridDim.x);
+        if (!dn && !STAGED) prefetch_tile(tile + gridDim.x);  // staged tiles arrive by TMA
         for (int j = 0; j < T; ++j, r.next()) {
           if (dn) CSB_TL(0, 30, j);
           rwait(&empty[r.idx], r.phase ^ 1);
           if (dn) CSB_TL(0, 31, j);
           ptx::mbar_arrive_expect_tx_elect(&full[r.idx], bytes);
-          ptx::bulk_g2s_elect(ring + r.idx * bytes, src + static_cast<size_t>(j) * bytes, bytes, &full[r.idx]);
+          if (CL > 1) {
+            const uint32_t slice = bytes / CL;
+            ptx::bulk_g2s_multicast_elect(ring + r.idx * bytes + cl_rank * slice,
+                                          src + static_cast<size_t>(j) * bytes + cl_rank * slice, slice,
+                                          &full[r.idx], cl_mask);
+          } else {
+            ptx::bulk_g2s_elect(ring + r.idx * bytes, src + static_cast<size_t>(j) * bytes, bytes, &full[r.idx]);
+          }
         }
       }
     }
@@ -333,7 +355,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           al += 8;
         }
         ptx::tc_commit_elect(&acc_full[b]);
-        ptx::tc_commit_elect(&dn_empty[rd.idx]);
+        if (CL > 1) {
+          ptx::tc_commit_multicast_elect(&dn_empty[rd.idx], cl_mask);
+        } else {
+          ptx::tc_commit_elect(&dn_empty[rd.idx]);
+        }
         if (j == T - 1) {
           ptx::tc_commit_elect(x_free);
           ++tcount1;
@@ -368,7 +394,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         } else {
           ptx::tc_commit_elect(&s_free[b]);
         }
-        ptx::tc_commit_elect(&p_empty[rp.idx]);
+        if (CL > 1) {
+          ptx::tc_commit_multicast_elect(&p_empty[rp.idx], cl_mask);
+        } else {
+          ptx::tc_commit_elect(&p_empty[rp.idx]);
+        }
         if (j == T - 1) {
           ptx::tc_commit_elect(o_full);
           ++tcount2;
@@ -384,10 +414,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       // only its own warp's MMAs, and all cross-GEMM dependencies are
       // mbarriers (ACC, S, X, O), so the tensor pipe may interleave freely.
       if (warp == 2) {
-        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+        for (int tile = blockIdx.x; tile < tile_end; tile += gridDim.x)
           for (int j = 0; j < T; ++j) issue_g1(j);
       } else {
-        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+        for (int tile = blockIdx.x; tile < tile_end; tile += gridDim.x)
           for (int j = 0; j < T; ++j) issue_g2(j);
       }
     }
@@ -398,17 +428,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int set = NB == 2 ? (ew >> 3) : 0;                // step parity owned
     const int half = NB == 2 ? ((ew >> 2) & 1) : (ew >> 2);  // column slice in step
-    // Tile boundary: with two step sets (NB = 2) the set that does NOT run
-    // the tile's last step stages the next tile's x (prologue) while the set
-    // that does reads O out, so the two run side by side; with one set all 16
-    // warps do both in turn.  Each role is kBW warps = kBG groups of four
-    // (one warp per TMEM lane quarter); gi is this warp's group.
-    constexpr int kBW = kSplit ? kSetWarps : kEpiWarps;
+    // Tile boundary (x prologue of the next tile, O readout of this one):
+    // all kBW = 16 epilogue warps, kBG = 4 groups of four (one warp per TMEM
+    // lane quarter); gi is this warp's group.
+    constexpr int kBW = kEpiWarps;
     constexpr int kBG = kBW / 4;
-    const int last_set = kSplit ? ((T - 1) & 1) : 0;
-    const bool does_readout = !kSplit || set == last_set;
-    const bool does_prologue = !kSplit || set != last_set;
-    const int gi = (ew >> 2) & (kBG - 1);
+    const int gi = ew >> 2;
     const int row = 32 * q + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     const IO* obs = static_cast<const IO*>(p.obs);
@@ -462,59 +487,96 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         ptx::mbar_wait(bar, parity);
       }
     };
+    // TMA issuer for the staged tile edge: one fixed thread (bulk groups are per thread)
+    const bool issuer_thread = ew == 0 && lane == 0;
+    float* s_stage = reinterpret_cast<float*>(smem + p.stage_out_off);  // halves A, B: [n][128] each
+    const uint32_t xs_bytes = static_cast<uint32_t>(p.n) * kObsTile * 4;
+    auto tma_x = [&](int tile_k, float* dst, uint64_t* bar) {
+      const int tk = min(tile_k, n_tiles - 1);  // a dummy slot reads a real tile (rows unused)
+      ptx::mbar_arrive_expect_tx(bar, xs_bytes);
+      ptx::tma_load_2d(dst, &p.tmap_obs, tk * kObsTile, 0, bar);
+    };
     uint32_t prologue_count = 0;
     // x prologue: warp group gi normalises, splits and stores K-chunks
-    // k8 = gi mod kBG and contributes a partial ||x||^2 for its chunks.  All
-    // loads of a batch are issued before any is consumed (one HBM latency
-    // per batch instead of one per chunk).  Column n + 1 of the operand is
+    // k8 = gi mod kBG and contributes a partial ||x||^2 for its chunks.
+    // Column n + 1 of the operand is
     // ||x||^2 / kXxCol (GEMM1 then yields d2 itself): it is written once the
     // partials are summed.  Returns ||x||^2 of this thread's row and whether
     // the row must be recomputed exactly.
     constexpr int PB = sizeof(IO) == 8 ? 2 : 4;  // chunks per load batch
     const uint32_t w_xx = static_cast<uint32_t>(p.n + 1) / 2;  // f16x2 word holding column n + 1
     auto prologue = [&](int tile, bool& bad_row) -> float {
-      CSB_TL(2 + (ew >> 3), 20, tile);
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 20, tile);
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
       float acc = 0.f;
       bool bad = false;  // a value outside the FP16 split's range: recompute the row exactly
       bool waited = false;
       const int kt = tile / static_cast<int>(gridDim.x);  // tile index of this CTA
-      for (int k0 = gi; k0 < K1 / 8; k0 += kBG * PB) {
-        float xv[PB][8];
-        {
-          IO raw[PB][8];
+      const float* xs = nullptr;
+      if constexpr (STAGED) {
+        wait(xa_full, kt & 1);
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 45, tile);
+        xs = s_stage;
+      }
+      // split and store one normalised 8-column chunk of the operand
+      auto put_chunk = [&](int k8, float* xv) {
+        uint32_t hi[4], lo[4];
 #pragma unroll
-          for (int b = 0; b < PB; ++b)
-            if (k0 + kBG * b < K1 / 8) load_chunk(t, valid, min(k0 + kBG * b, (p.n - 1) / 8), raw[b]);
-#pragma unroll
-          for (int b = 0; b < PB; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) xv[b][e] = norm(raw[b][e], (k0 + kBG * b) * 8 + e, valid);
-        }
-        if (!waited) {
-          wait(x_free, (prologue_count & 1) ^ 1);
-          ++prologue_count;
-          ptx::tc_fence_after();
-          CSB_TL(2 + (ew >> 3), 21, tile);
-          waited = true;
+        for (int e = 0; e < 8; ++e) {
+          if (k8 * 8 + e < p.n) acc = fmaf(xv[e], xv[e], acc);
+          const bool out = !(fabsf(xv[e]) < kF16Safe);
+          bad |= out;
+          if (out) xv[e] = 0.f;
         }
 #pragma unroll
-        for (int b = 0; b < PB; ++b) {
-          const int k8 = k0 + kBG * b;
-          if (k8 >= K1 / 8) break;
-          uint32_t hi[4], lo[4];
+        for (int e = 0; e < 4; ++e) ptx::split_f16x2(xv[2 * e], xv[2 * e + 1], hi[e], lo[e]);
+        ptx::tmem_st4(tmem + lane_off + colXh + k8 * 4, hi);
+        ptx::tmem_st4(tmem + lane_off + colXl + k8 * 4, lo);
+      };
+      if (xs) {
+        // staged: shared-memory reads, one chunk at a time (no load batches
+        // to keep live: batched registers spilled, and with ~220 KB of
+        // shared memory the spills missed the small L1)
+        wait(x_free, (prologue_count & 1) ^ 1);
+        ++prologue_count;
+        ptx::tc_fence_after();
+        waited = true;
+        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 21, tile);
+        for (int k8 = gi; k8 < K1 / 8; k8 += kBG) {
+          float xv[8];
+          const int c = min(k8, (p.n - 1) / 8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            if (k8 * 8 + e < p.n) acc = fmaf(xv[b][e], xv[b][e], acc);
-            const bool out = !(fabsf(xv[b][e]) < kF16Safe);
-            bad |= out;
-            if (out) xv[b][e] = 0.f;
+          for (int e = 0; e < 8; ++e) xv[e] = norm(xs[min(c * 8 + e, p.n - 1) * kObsTile + row], k8 * 8 + e, valid);
+          put_chunk(k8, xv);
+        }
+      } else {
+        // global loads: all loads of a batch are issued before any is
+        // consumed (one memory latency per batch instead of one per chunk)
+        for (int k0 = gi; k0 < K1 / 8; k0 += kBG * PB) {
+          float xv[PB][8];
+          {
+            IO raw[PB][8];
+#pragma unroll
+            for (int b = 0; b < PB; ++b)
+              if (k0 + kBG * b < K1 / 8) load_chunk(t, valid, min(k0 + kBG * b, (p.n - 1) / 8), raw[b]);
+#pragma unroll
+            for (int b = 0; b < PB; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) xv[b][e] = norm(raw[b][e], (k0 + kBG * b) * 8 + e, valid);
+          }
+          if (!waited) {
+            wait(x_free, (prologue_count & 1) ^ 1);
+            ++prologue_count;
+            ptx::tc_fence_after();
+            if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 21, tile);
+            waited = true;
           }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) ptx::split_f16x2(xv[b][2 * e], xv[b][2 * e + 1], hi[e], lo[e]);
-          ptx::tmem_st4(tmem + lane_off + colXh + k8 * 4, hi);
-          ptx::tmem_st4(tmem + lane_off + colXl + k8 * 4, lo);
+          for (int b = 0; b < PB; ++b) {
+            if (k0 + kBG * b >= K1 / 8) break;
+            put_chunk(k0 + kBG * b, xv[b]);
+          }
         }
       }
       if (!waited) {
@@ -523,11 +585,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         ptx::tc_fence_after();
       }
       const int par = kt & 1;
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 42, tile);
       float* xx_part = s_xx + par * 4 * kObsTile;
       uint8_t* bad_part = s_bad + par * 4 * kObsTile;
       xx_part[gi * kObsTile + row] = acc;
       bad_part[gi * kObsTile + row] = bad && valid;
       ptx::named_bar_sync(1, kBW * 32);
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 43, tile);
       float xx = 0.f;
 #pragma unroll
       for (int g = 0; g < kBG; ++g) {
@@ -536,14 +600,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       }
       const float xc = xx * (1.f / kXxCol);
       bad = (bad || !(xc < kF16Safe)) && valid;
-      if (kSplit && gi == 0) {
-        // hand ||x||^2 to the readout set once it has taken the previous one
-        if (kt >= 1) wait(xx_taken, (kt - 1) & 1);
-        s_xx_tot[row] = xx;
-        s_bad_tot[row] = bad;
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(xx_posted);
-      }
       if (gi == 0) {
         // the word holding column n + 1 (its partner is the ||d||^2 column n
         // or the zero column n + 2)
@@ -561,7 +617,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       ptx::tc_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
-      CSB_TL(2 + (ew >> 3), 22, tile);
+      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 22, tile);
       if (lane == 0) ptx::mbar_arrive(x_ready);
       bad_row = bad;
       return xx;
@@ -573,32 +629,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     // every d2 >= thr clears the exact near-zero criterion; thr > 0, so rows
     // whose minimum passes also need no clamp before the square root
     auto set_thr = [&]() { thr_cur = p.tau * (xx_cur + p.dd_max); };
-    // TMA store issuer: one fixed thread of the readout role (bulk groups are per thread)
-    const bool issuer_thread = does_readout && ew % kBW == 0 && lane == 0;
-    // ||x||^2 of the row for tile index k (per CTA), staged by the prologue set
-    auto fetch_xx = [&](int k) {
-      wait(xx_posted, k & 1);
-      xx_cur = s_xx_tot[row];
-      bad_cur = s_bad_tot[row] != 0;
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(xx_taken);
+    if (n_iter > 0) {
+      if (STAGED && issuer_thread) tma_x(blockIdx.x, s_stage, xa_full);  // x(0) for the first prologue
+      xx_cur = prologue(blockIdx.x, bad_cur);
       set_thr();
-    };
-    if (static_cast<int>(blockIdx.x) < n_tiles) {
-      if (does_prologue) {
-        xx_cur = prologue(blockIdx.x, bad_cur);
-        set_thr();
-      } else {
-        fetch_xx(0);
-      }
     }
     const float inv_h_s = p.inv_h * (1.f / kSScale);  // exact power-of-two rescaling
     const uint32_t a_base = colAcc + set * MT + c0;
     const int sbuf = SB == 2 ? set : 0;
     const uint32_t s_base = colS + sbuf * MT + c0 / 2;  // f16x2: two columns per word
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+    for (int tile = blockIdx.x; tile < tile_end; tile += gridDim.x, ++tcount) {
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
+      bool x_due = STAGED && issuer_thread;
       for (int j = set; j < T; j += NB, ++use) {
         const int valid_cols = min(COLS, p.m - (j * MT + c0));
         const float* dd = p.dd + static_cast<size_t>(j) * MT + c0;
@@ -712,6 +755,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           // two steps ahead overlaps the kernel map), then map and store S
           float vall[COLS];
           load_acc(vall);
+          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 46, j);
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
@@ -730,62 +774,84 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         __syncwarp();
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 14, j);
         if (lane == 0) ptx::mbar_arrive(&s_ready[sbuf]);
+        if (x_due) {  // staged issuer, first step of the tile: stage x(k + 1) and x(k)
+          ptx::bulk_wait_read0();  // the previous edge's stores have read both halves
+          ptx::fence_proxy_async_smem();
+          if (tile + static_cast<int>(gridDim.x) < tile_end) tma_x(tile + gridDim.x, s_stage, xa_full);
+          tma_x(tile, s_stage + p.n * kObsTile, xb_full);
+          x_due = false;
+        }
       }
       // next tile's x prologue overlaps this tile's last GEMM2
       const int next = tile + gridDim.x;
       float xx_next = 0.f;
       bool bad_next = false;
-      if (does_prologue && next < n_tiles) xx_next = prologue(next, bad_next);
+      if (next < tile_end) xx_next = prologue(next, bad_next);
 
       // readout: estimate = scale .* O, residual = x - estimate.  The raw
       // observations of a batch are loaded before waiting for O.
       const bool issuer = issuer_thread;
-      if (does_readout) {
+      {
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
-        float* s_out = reinterpret_cast<float*>(smem + p.stage_out_off);  // [2][n][128]
-        if (p.staged) {
-          // the previous tile's TMA stores must have read the staging area
-          if (issuer) ptx::bulk_wait_read0();
-          ptx::named_bar_sync(2, kBW * 32);
-        }
-        // x loads of all of a thread's chunks are issued before O is waited
-        // for (one latency); O is read a chunk at a time (register pressure)
-        constexpr int RB = kBG == 4 ? PB : 2;
+        float* s_out = s_stage;  // est -> half A, resid -> half B (over x)
         bool o_ready = false;
-        for (int cb = gi; cb < N2 / 8; cb += kBG * RB) {
-          IO xr[RB][8];
-#pragma unroll
-          for (int b = 0; b < RB; ++b)
-            if (cb + kBG * b < N2 / 8) load_chunk(t, valid, min(cb + kBG * b, (p.n - 1) / 8), xr[b]);
-          if (!o_ready) {
+        if constexpr (STAGED) {
+          {
+            // x(k) is in half B: one chunk at a time from shared memory
+            float* xb = s_stage + p.n * kObsTile;
+            wait(xb_full, tcount & 1);
             wait(o_full, tcount & 1);
             ptx::tc_fence_after();
             if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
             o_ready = true;
+            for (int c = gi; c < N2 / 8; c += kBG) {
+              float o[8];
+              ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+              if ((ew & 7) == 0 && c == gi) CSB_TL(2 + (ew >> 3), 44, tile);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int s = c * 8 + e;
+                if (s < p.n) {
+                  const float ev = o[e] * s_scale_f[s];
+                  s_out[s * kObsTile + row] = ev;
+                  xb[s * kObsTile + row] -= ev;
+                }
+              }
+            }
           }
+        } else {
+          // x loads of all of a thread's chunks are issued before O is waited
+          // for (one latency); O is read a chunk at a time (register pressure)
+          constexpr int RB = kBG == 4 ? PB : 2;
+          for (int cb = gi; cb < N2 / 8; cb += kBG * RB) {
+            IO xr[RB][8];
 #pragma unroll
-          for (int b = 0; b < RB; ++b) {
-            const int c = cb + kBG * b;
-            if (c >= N2 / 8) break;
-            float o[8];
-            ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+            for (int b = 0; b < RB; ++b)
+              if (cb + kBG * b < N2 / 8) load_chunk(t, valid, min(cb + kBG * b, (p.n - 1) / 8), xr[b]);
+            if (!o_ready) {
+              wait(o_full, tcount & 1);
+              ptx::tc_fence_after();
+              if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
+              o_ready = true;
+            }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int s = c * 8 + e;
-              const bool ok = valid && s < p.n;
-              const int64_t idx = t + static_cast<int64_t>(s) * p.ld;
-              if constexpr (sizeof(IO) == 8) {
-                const double ev = static_cast<double>(o[e]) * s_scale_d[s];
-                if (ok && est) est[idx] = ev;
-                if (ok && resid) resid[idx] = xr[b][e] - ev;
-              } else {
-                const float ev = o[e] * s_scale_f[s];
-                if (p.staged) {
-                  if (s < p.n) {
-                    s_out[s * kObsTile + row] = ev;
-                    s_out[(p.n + s) * kObsTile + row] = xr[b][e] - ev;
-                  }
+            for (int b = 0; b < RB; ++b) {
+              const int c = cb + kBG * b;
+              if (c >= N2 / 8) break;
+              float o[8];
+              ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
+              if ((ew & 7) == 0 && c == gi) CSB_TL(2 + (ew >> 3), 44, tile);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int s = c * 8 + e;
+                const bool ok = valid && s < p.n;
+                const int64_t idx = t + static_cast<int64_t>(s) * p.ld;
+                if constexpr (sizeof(IO) == 8) {
+                  const double ev = static_cast<double>(o[e]) * s_scale_d[s];
+                  if (ok && est) est[idx] = ev;
+                  if (ok && resid) resid[idx] = xr[b][e] - ev;
                 } else {
+                  const float ev = o[e] * s_scale_f[s];
                   if (ok && est) est[idx] = ev;
                   if (ok && resid) resid[idx] = xr[b][e] - ev;
                 }
@@ -801,10 +867,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(o_free);  // O read: the next tile's GEMM2 may start
-        if (p.staged) {
+        if constexpr (STAGED) {
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(2, kBW * 32);
-          if (issuer) {
+          if (issuer && tile < n_tiles) {  // (a dummy slot has nothing to store)
             const int t0 = tile * kObsTile;
             if (est) ptx::tma_store_2d(&p.tmap_est, t0, 0, s_out);
             if (resid) ptx::tma_store_2d(&p.tmap_res, t0, 0, s_out + p.n * kObsTile);
@@ -813,20 +879,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         }
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
       }
-      if (next < n_tiles) {
-        if (does_prologue) {
-          xx_cur = xx_next;
-          bad_cur = bad_next;
-          set_thr();
-        } else {
-          fetch_xx(tcount + 1);
-        }
+      if (next < tile_end) {
+        xx_cur = xx_next;
+        bad_cur = bad_next;
+        set_thr();
       }
       if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 26, tile);
     }
-    if (p.staged && issuer_thread) ptx::bulk_wait0();  // stores complete before exit
+    if (STAGED && issuer_thread) ptx::bulk_wait0();  // stores complete before exit
   }
   __syncthreads();
+  if (CL > 1) ptx::cluster_sync();  // no CTA leaves while peers may still signal it
   if (warp == 0) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kTmemCols);

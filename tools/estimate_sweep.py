@@ -39,7 +39,11 @@ def main():
             p.estimate_device(g, d_obs, d_est, d_res, st)
         times = []
         for _ in range(10):
-            flush.zero_()
+            mode = os.environ.get("FLUSH", "write")
+            if mode == "write":
+                flush.zero_()
+            elif mode == "read":
+                flush.sum(dtype=torch.int32)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(st)

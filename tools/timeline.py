@@ -22,7 +22,7 @@ CAP = 8192
 NAMES = {1: "g1.enter", 2: "g1.issue", 3: "g2.enter", 4: "g2.issue",
          10: "epi.acc_wait", 11: "epi.acc_got", 12: "epi.computed", 13: "epi.sfree_got", 14: "epi.stored",
          20: "pro.enter", 21: "pro.xfree_got", 22: "pro.done", 23: "rd.ofull_wait", 24: "rd.ofull_got",
-         25: "rd.done", 26: "rd.gathered", 27: "rd.looped", 30: "prod.dn_wait", 31: "prod.dn_got", 33: "prod.p_got"}
+         25: "rd.done", 26: "rd.gathered", 27: "rd.looped", 40: "pro.loaded", 42: "pro.stored", 43: "pro.barrier", 44: "rd.tmem1", 45: "pro.xa_got", 46: "epi.acc_loaded", 30: "prod.dn_wait", 31: "prod.dn_got", 33: "prod.p_got"}
 SLOTS = {0: "producer", 1: "mma g1", 2: "epi set0", 3: "epi set1", 4: "mma g2"}
 
 

@@ -434,7 +434,7 @@ def run_b200(args, world, rank, local):
     achieved_tflops = flops_per_obs * N_OBS / (mean_ms * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops", 1590.0)
     # tensor work actually issued: 3 FP16 products per GEMM incl. padding
-    K1, N2 = (N_SIG + 1 + 15) // 16 * 16, (N_SIG + 15) // 16 * 16
+    K1, N2 = (N_SIG + 2 + 15) // 16 * 16, (N_SIG + 15) // 16 * 16  # + ||d||^2, ||x||^2 columns
     MT = 64  # tile the library selects for n = 100 (choose_tc_shape: MT 64, 2 ACC + 2 S buffers)
     f16_peak = load_f16_peak() or 2380.0
     m_pad = (N_MEM + MT - 1) // MT * MT
@@ -467,7 +467,7 @@ def run_b200(args, world, rank, local):
                 "api": "cs_mset_estimate (pinned host FP64 in, estimates + residuals out)"},
         "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": bf16, "unit": "TFLOP/s",
                      "frac": achieved_tflops / bf16, "traffic": traffic,
-                     "kernel": "mset_estimate_tc_kernel<64,2,2,float>",
+                     "kernel": "mset_estimate_tc_kernel<64,2,2,float,true>",
                      "algorithmic_flops_per_launch": flops_per_obs * N_OBS,
                      "peak_note": "peak = measured dense bf16 (MEASURED_PEAKS.json); the kernel runs "
                                   "tcgen05 kind::f16 (same dense rate) and issues 3 split products per "

@@ -3,7 +3,7 @@
 
 Workload (per GPU): n = 100 signals, N = 100,000 surveillance observations,
 m = 1,000 memory vectors, 4,000 training rows; FP64 train + FP32 (tcgen05
-3xTF32) surveillance; inverse-distance kernel, h = sqrt(n); synthetic data
+3xFP16) surveillance; inverse-distance kernel, h = sqrt(n); synthetic data
 from the reference's synthesis recipe (demo template: phi 0.5, rho 0.3,
 var 1, skew 0.5, kurt 4, master seed 20260810).
 

@@ -57,7 +57,7 @@ enum { CS_KERNEL_INVERSE_DISTANCE = 0, CS_KERNEL_GAUSSIAN = 1 };
  *    FMA contraction -- bit-identical to the CPU reference given the same model.
  *  CS_PRECISION_FP32: reassociated est = P S with P = D_norm G+ formed once at
  *    train time in FP64, distance and weight GEMMs on tcgen05
- *    tensor cores as 3xTF32 split products (FP32-accurate), kernel map fused
+ *    tensor cores as 3xFP16 split products (FP32-accurate), kernel map fused
  *    in the epilogue.  Tolerance 1e-3 relative to max|estimate| (north_star). */
 enum { CS_PRECISION_FP64 = 0, CS_PRECISION_FP32 = 1 };
 

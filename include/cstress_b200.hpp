@@ -102,7 +102,7 @@ struct KernelConfig {
 // ----------------------------------------------------------- backends.hpp
 struct BackendId {
   int device = 0;
-  int precision = CS_PRECISION_FP64;  // CS_PRECISION_FP32: tcgen05 3xTF32 surveillance
+  int precision = CS_PRECISION_FP64;  // CS_PRECISION_FP32: tcgen05 3xFP16 surveillance
   static BackendId b200(int device = 0, int precision = CS_PRECISION_FP64) { return {device, precision}; }
   std::string label() const {
     return "b200[device=" + std::to_string(device) + "/precision=" +

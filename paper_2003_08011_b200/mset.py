@@ -62,7 +62,7 @@ class BackendId:
 
     ``precision`` selects the surveillance arithmetic: ``fp64`` reproduces
     the reference's association and summation order bit-for-bit;
-    ``fp32`` runs the fused tcgen05 3xTF32 kernel (tolerance 1e-3).
+    ``fp32`` runs the fused tcgen05 3xFP16 kernel (tolerance 1e-3).
     """
     kind: str = "b200"
     device: int = 0

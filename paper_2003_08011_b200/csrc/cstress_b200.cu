@@ -681,6 +681,10 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
       if (resid) ok = ok && encode_out_map(&p.tmap_res, resid, N, static_cast<int>(M->n), ld);
       if (ok) {
         p.staged = 1;
+        // split tile edge: measured 3-8% faster for short memory loops
+        // (n=20: T=2, n=64: T=8) and 1% slower at C2 (T=16)
+        p.split_edge = M->m_tiles <= 12 ? 1 : 0;
+        if (const char* e = std::getenv("CSB_SPLIT_EDGE")) p.split_edge = e[0] == '1';
       } else {
         p.n_stages = M->n_stages;
         smem = M->n_stages * stage + tc_aux_bytes(p.K1);

@@ -83,6 +83,7 @@ struct TcParams {
   // per-thread loads the x prologue and readout each waited ~6k cycles on
   // spilled load batches.
   int staged;
+  int split_edge;          // staged, NB = 2: split the tile edge between the step sets
   uint32_t stage_out_off;  // byte offset of the staging area
   CUtensorMap tmap_obs, tmap_est, tmap_res;
 };
@@ -131,6 +132,10 @@ __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
 #ifndef CSB_RCP_MUFU
 #define CSB_RCP_MUFU 2
 #endif
+// staged readout: 8-column O chunks read per TMEM load wait
+#ifndef CSB_RD_BATCH
+#define CSB_RD_BATCH 2
+#endif
 #ifndef CSB_WAIT_SLEEP
 #define CSB_WAIT_SLEEP 0
 #endif
@@ -157,6 +162,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   static_assert(NB == 1 || NB == 2, "one or two TMEM buffers");
   static_assert(SB >= 1 && SB <= NB, "S buffers");
   static_assert(!STAGED || sizeof(IO) == 4, "staged tile edge: FP32 I/O");
+  // Staged, two step sets, p.split_edge: the tile edge is split between the
+  // sets -- the set that does not own the last step stages the next tile's x
+  // (it is done with the tile first), the other reads O out; see the epilogue.
+  const bool kSplitEdge = STAGED && NB == 2 && p.split_edge;
   constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
   constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
   constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
@@ -189,12 +198,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
   uint64_t* xa_full = bars + 29;  // staged: x of the next tile in staging half A
   uint64_t* xb_full = bars + 30;  // staged: x of this tile in staging half B
+  uint64_t* a_done = bars + 31;   // split edge: prologue done with half A, ||x||^2 posted
+  uint64_t* g2_last = bars + 32;  // GEMM2 of a tile's last step has been issued
   double* s_inv_d = reinterpret_cast<double*>(bars + 64);
   double* s_scale_d = s_inv_d + p.K1;
   float* s_inv_f = reinterpret_cast<float*>(s_scale_d + p.K1);
   float* s_scale_f = s_inv_f + p.K1;
   float* s_xx = s_scale_f + p.K1;  // [2][4][kObsTile] ||x||^2 partials (by tile parity)
   uint8_t* s_bad = reinterpret_cast<uint8_t*>(s_xx + 2 * 4 * kObsTile);  // [2][4][kObsTile] out-of-range flags
+  float* s_xx_tot = reinterpret_cast<float*>(s_bad + 2 * 4 * kObsTile);  // [2][kObsTile] split edge: ||x||^2 per row
+  uint8_t* s_bad_tot = reinterpret_cast<uint8_t*>(s_xx_tot + 2 * kObsTile);  // [2][kObsTile]
 
   // Thread-block cluster of CL CTAs (CL = 1 without a cluster launch): the
   // operand tiles are identical for every CTA, so each CTA's producer copies
@@ -213,12 +226,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       ptx::mbar_init(&s_ready[b], kSetWarps);
       ptx::mbar_init(&s_free[b], 1);
     }
-    ptx::mbar_init(x_ready, kEpiWarps);
+    ptx::mbar_init(x_ready, kSplitEdge ? kSetWarps : kEpiWarps);
     ptx::mbar_init(x_free, 1);
     ptx::mbar_init(o_full, 1);
     ptx::mbar_init(xa_full, 1);
     ptx::mbar_init(xb_full, 1);
-    ptx::mbar_init(o_free, kEpiWarps);
+    ptx::mbar_init(o_free, kSplitEdge ? kSetWarps : kEpiWarps);
+    ptx::mbar_init(a_done, 4);
+    ptx::mbar_init(g2_last, 1);
     ptx::fence_mbar_init();
   }
   for (int s = threadIdx.x; s < p.K1; s += blockDim.x) {
@@ -336,7 +351,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       auto issue_g1 = [&](int j) {
         const int b = NB == 2 ? (j & 1) : 0;
         CSB_TL(1, 1, j);
-        if (j == 0) rwait(x_ready, tcount1 & 1);
+        if (j == 0) {
+          rwait(x_ready, tcount1 & 1);
+          // the tensor pipe runs MMAs in issue order: the next tile's GEMM1
+          // goes after this tile's last GEMM2, whose completion (o_full)
+          // starts the readout on the critical path
+          if (tcount1 > 0) rwait(g2_last, (tcount1 - 1) & 1);
+        }
         rwait(&dn_full[rd.idx], rd.phase);
         rwait(&acc_free[b], (acc_use[b] & 1) ^ 1);
         ptx::tc_fence_after();
@@ -401,6 +422,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         }
         if (j == T - 1) {
           ptx::tc_commit_elect(o_full);
+          ptx::mbar_arrive_elect(g2_last);
           ++tcount2;
         }
         ++s_use[b];
@@ -428,12 +450,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int set = NB == 2 ? (ew >> 3) : 0;                // step parity owned
     const int half = NB == 2 ? ((ew >> 2) & 1) : (ew >> 2);  // column slice in step
-    // Tile boundary (x prologue of the next tile, O readout of this one):
-    // all kBW = 16 epilogue warps, kBG = 4 groups of four (one warp per TMEM
-    // lane quarter); gi is this warp's group.
-    constexpr int kBW = kEpiWarps;
-    constexpr int kBG = kBW / 4;
-    const int gi = ew >> 2;
+    // Tile edge (x prologue of the next tile, O readout of this one).  Split
+    // edge: the set that does not own step T-1 runs the prologue (8 warps)
+    // while the owner of T-1 finishes it and reads O out (8 warps); the
+    // prologue set posts ||x||^2 per row through shared memory (a_done).
+    // Otherwise all 16 warps run both in turn.  A role is kBW warps = kBG
+    // groups of four (one warp per TMEM lane quarter); gi is this warp's group.
+    const int kBW = kSplitEdge ? kSetWarps : kEpiWarps;
+    const int kBG = kBW / 4;
+    const int gi = (ew >> 2) & (kBG - 1);
+    const int last_set = kSplitEdge ? ((T - 1) & 1) : 0;
+    const bool do_pro = !kSplitEdge || set != last_set;
+    const bool do_read = !kSplitEdge || set == last_set;
     const int row = 32 * q + lane;
     const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
     const IO* obs = static_cast<const IO*>(p.obs);
@@ -488,7 +516,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       }
     };
     // TMA issuer for the staged tile edge: one fixed thread (bulk groups are per thread)
-    const bool issuer_thread = ew == 0 && lane == 0;
+    const bool issuer_thread = do_read && ew % kBW == 0 && lane == 0;
     float* s_stage = reinterpret_cast<float*>(smem + p.stage_out_off);  // halves A, B: [n][128] each
     const uint32_t xs_bytes = static_cast<uint32_t>(p.n) * kObsTile * 4;
     auto tma_x = [&](int tile_k, float* dst, uint64_t* bar) {
@@ -600,6 +628,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       }
       const float xc = xx * (1.f / kXxCol);
       bad = (bad || !(xc < kF16Safe)) && valid;
+      if (kSplitEdge && gi == 0) {
+        s_xx_tot[par * kObsTile + row] = xx;
+        s_bad_tot[par * kObsTile + row] = bad;
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(a_done);  // (after the barrier: all reads of A done)
+      }
       if (gi == 0) {
         // the word holding column n + 1 (its partner is the ||d||^2 column n
         // or the zero column n + 2)
@@ -629,10 +663,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     // every d2 >= thr clears the exact near-zero criterion; thr > 0, so rows
     // whose minimum passes also need no clamp before the square root
     auto set_thr = [&]() { thr_cur = p.tau * (xx_cur + p.dd_max); };
+    // split edge, readout set: ||x||^2 of tile index k posted by the prologue set
+    auto fetch_xx = [&](int k) {
+      wait(a_done, k & 1);
+      xx_cur = s_xx_tot[(k & 1) * kObsTile + row];
+      bad_cur = s_bad_tot[(k & 1) * kObsTile + row] != 0;
+      set_thr();
+    };
     if (n_iter > 0) {
       if (STAGED && issuer_thread) tma_x(blockIdx.x, s_stage, xa_full);  // x(0) for the first prologue
-      xx_cur = prologue(blockIdx.x, bad_cur);
-      set_thr();
+      if (do_pro) {
+        xx_cur = prologue(blockIdx.x, bad_cur);
+        set_thr();
+      } else {
+        fetch_xx(0);
+      }
     }
     const float inv_h_s = p.inv_h * (1.f / kSScale);  // exact power-of-two rescaling
     const uint32_t a_base = colAcc + set * MT + c0;
@@ -786,12 +831,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       const int next = tile + gridDim.x;
       float xx_next = 0.f;
       bool bad_next = false;
-      if (next < tile_end) xx_next = prologue(next, bad_next);
+      if (do_pro && next < tile_end) xx_next = prologue(next, bad_next);
 
       // readout: estimate = scale .* O, residual = x - estimate.  The raw
       // observations of a batch are loaded before waiting for O.
       const bool issuer = issuer_thread;
-      {
+      if (do_read) {
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
         float* s_out = s_stage;  // est -> half A, resid -> half B (over x)
         bool o_ready = false;
@@ -800,21 +845,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             // x(k) is in half B: one chunk at a time from shared memory
             float* xb = s_stage + p.n * kObsTile;
             wait(xb_full, tcount & 1);
+            // half A holds x(k + 1) until the prologue set has staged it
+            if (kSplitEdge && next < tile_end) wait(a_done, (tcount + 1) & 1);
             wait(o_full, tcount & 1);
             ptx::tc_fence_after();
             if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
             o_ready = true;
-            for (int c = gi; c < N2 / 8; c += kBG) {
-              float o[8];
-              ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
-              if ((ew & 7) == 0 && c == gi) CSB_TL(2 + (ew >> 3), 44, tile);
+            // O read CSB_RD_BATCH chunks per TMEM wait
+            constexpr int OB = CSB_RD_BATCH;
+            for (int c0 = gi; c0 < N2 / 8; c0 += OB * kBG) {
+              float o[OB][8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int s = c * 8 + e;
-                if (s < p.n) {
-                  const float ev = o[e] * s_scale_f[s];
-                  s_out[s * kObsTile + row] = ev;
-                  xb[s * kObsTile + row] -= ev;
+              for (int b = 0; b < OB; ++b)
+                if (c0 + b * kBG < N2 / 8) ptx::tmem_ld8(tmem + lane_off + colO + (c0 + b * kBG) * 8, o[b]);
+              ptx::tc_wait_ld();
+              if ((ew & 7) == 0 && c0 == gi) CSB_TL(2 + (ew >> 3), 44, tile);
+#pragma unroll
+              for (int b = 0; b < OB; ++b) {
+                const int c = c0 + b * kBG;
+                if (c >= N2 / 8) break;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int s = c * 8 + e;
+                  if (s < p.n) {
+                    const float ev = o[b][e] * s_scale_f[s];
+                    s_out[s * kObsTile + row] = ev;
+                    xb[s * kObsTile + row] -= ev;
+                  }
                 }
               }
             }
@@ -822,7 +879,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         } else {
           // x loads of all of a thread's chunks are issued before O is waited
           // for (one latency); O is read a chunk at a time (register pressure)
-          constexpr int RB = kBG == 4 ? PB : 2;
+          constexpr int RB = PB;  // (plain edge: four groups)
           for (int cb = gi; cb < N2 / 8; cb += kBG * RB) {
             IO xr[RB][8];
 #pragma unroll
@@ -880,9 +937,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
       }
       if (next < tile_end) {
-        xx_cur = xx_next;
-        bad_cur = bad_next;
-        set_thr();
+        if (do_pro) {
+          xx_cur = xx_next;
+          bad_cur = bad_next;
+          set_thr();
+        } else {
+          fetch_xx(tcount + 1);
+        }
       }
       if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 26, tile);
     }

@@ -270,21 +270,45 @@ bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
   const CusolverApi& api = cusolver_api();
   if (!ctx->solver) solver_check(api.create(&ctx->solver), "cusolverDnCreate");
   solver_check(api.set_stream(ctx->solver, st), "SetStream");
-  CSB_CUDA(cudaMemcpyAsync(out, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
   const int mi = static_cast<int>(m);
-  int l1 = 0, l2 = 0;
-  solver_check(api.potrf_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, &l1), "Dpotrf_bufferSize");
-  solver_check(api.potri_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, &l2), "Dpotri_bufferSize");
-  TmpBuf<double> work(static_cast<size_t>(std::max(l1, l2)) + 1);
-  TmpBuf<int> info(2);
-  solver_check(api.potrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, work.get(), l1, info.get()),
-               "Dpotrf");
-  solver_check(api.potri(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, work.get(), l2, info.get() + 1),
-               "Dpotri");
-  int h[2] = {0, 0};
-  CSB_CUDA(cudaMemcpyAsync(h, info.get(), sizeof h, cudaMemcpyDeviceToHost, st));
-  CSB_CUDA(cudaStreamSynchronize(st));
-  if (h[0] != 0 || h[1] != 0) return false;
+  const char* env = std::getenv("CSB_POTRI");
+  if (env && env[0] == '1') {
+    // factor + potri (triangular inverse and L^-T L^-1 in place)
+    CSB_CUDA(cudaMemcpyAsync(out, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int l1 = 0, l2 = 0;
+    solver_check(api.potrf_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, &l1), "Dpotrf_bufferSize");
+    solver_check(api.potri_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, &l2), "Dpotri_bufferSize");
+    TmpBuf<double> work(static_cast<size_t>(std::max(l1, l2)) + 1);
+    TmpBuf<int> info(2);
+    solver_check(api.potrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, work.get(), l1, info.get()),
+                 "Dpotrf");
+    solver_check(api.potri(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, out, mi, work.get(), l2, info.get() + 1),
+                 "Dpotri");
+    int h[2] = {0, 0};
+    CSB_CUDA(cudaMemcpyAsync(h, info.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    if (h[0] != 0 || h[1] != 0) return false;
+  } else {
+    // factor, then G^-1 = potrs(L, I): two triangular solves with m
+    // right-hand sides (cuBLAS TRSM, ~2 m^3 flops at GEMM-like rates); the
+    // in-place potri (trtri + lauum) was ~8x slower at m = 1000-4000
+    TmpBuf<double> L(static_cast<size_t>(m) * m);
+    CSB_CUDA(cudaMemcpyAsync(L.get(), G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int l1 = 0;
+    solver_check(api.potrf_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, L.get(), mi, &l1), "Dpotrf_bufferSize");
+    TmpBuf<double> work(static_cast<size_t>(l1) + 1);
+    TmpBuf<int> info(2);
+    solver_check(api.potrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, L.get(), mi, work.get(), l1, info.get()),
+                 "Dpotrf");
+    set_identity_kernel<<<grid_for(m * m), 256, 0, st>>>(out, m);
+    CSB_LAUNCH_CHECK();
+    solver_check(api.potrs(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, mi, L.get(), mi, out, mi, info.get() + 1),
+                 "Dpotrs");
+    int h[2] = {0, 0};
+    CSB_CUDA(cudaMemcpyAsync(h, info.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    if (h[0] != 0 || h[1] != 0) return false;
+  }
   symmetrize_lower_kernel<<<grid_for(m * m), 256, 0, st>>>(out, m);
   CSB_LAUNCH_CHECK();
   return true;

@@ -289,8 +289,17 @@ __global__ void whiten_kernel(const double* __restrict__ V, const double* __rest
   }
 }
 
+// Column-major m x m identity (right-hand side of potrs for the inverse).
+__global__ void set_identity_kernel(double* __restrict__ A, int64_t m) {
+  const int64_t total = m * m;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    A[e] = (e % m == e / m) ? 1.0 : 0.0;
+}
+
 // Mirror the lower triangle into the upper one (potri writes the lower
-// triangle of the inverse only).
+// triangle of the inverse only; potrs's full result is made exactly
+// symmetric the same way).
 __global__ void symmetrize_lower_kernel(double* __restrict__ A, int64_t m) {
   const int64_t total = m * m;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;

@@ -36,6 +36,8 @@ struct CusolverApi {
   cusolverStatus_t (*potri_buffer)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, int*) = nullptr;
   cusolverStatus_t (*potri)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, double*, int,
                             int*) = nullptr;
+  cusolverStatus_t (*potrs)(cusolverDnHandle_t, cublasFillMode_t, int, int, const double*, int, double*, int,
+                            int*) = nullptr;
 };
 
 inline const CusolverApi& cusolver_api() {
@@ -74,8 +76,9 @@ inline const CusolverApi& cusolver_api() {
     api.potri_buffer =
         reinterpret_cast<decltype(api.potri_buffer)>(dlsym(api.lib, "cusolverDnDpotri_bufferSize"));
     api.potri = reinterpret_cast<decltype(api.potri)>(dlsym(api.lib, "cusolverDnDpotri"));
+    api.potrs = reinterpret_cast<decltype(api.potrs)>(dlsym(api.lib, "cusolverDnDpotrs"));
     if (!api.create || !api.destroy || !api.set_stream || !api.syevd_buffer || !api.syevd ||
-        !api.potrf_buffer || !api.potrf || !api.potri_buffer || !api.potri) {
+        !api.potrf_buffer || !api.potrf || !api.potri_buffer || !api.potri || !api.potrs) {
       error += "missing cuSOLVER symbols in " + api.path;
       api.lib = nullptr;
     }

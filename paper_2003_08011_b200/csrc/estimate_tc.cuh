@@ -130,7 +130,7 @@ __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
 // 1 epilogue, 2 every role; measured: 0 is as fast at C2 and 9% faster at
 // n = 20).
 #ifndef CSB_RCP_MUFU
-#define CSB_RCP_MUFU 2
+#define CSB_RCP_MUFU 4  // measured (C2, n=100/m=4000): 4 beats 2 by 3-8%, n=64 within 1.5%
 #endif
 // staged readout: 8-column O chunks read per TMEM load wait
 #ifndef CSB_RD_BATCH
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             // 2^14 / (1 + sqrt(d2)/h) = 1 / (2^-14 + sqrt(d2) (2^-14/h)): the
             // scale folds into the FMA exactly.  sqrt on the MUFU pipe; of
             // every four reciprocals CSB_RCP_MUFU go to MUFU, the rest to an
-            // FMA-pipe Newton iteration, so the two pipes share the work.
+            // FMA-pipe Newton iteration (default: all on MUFU).
 #pragma unroll
             for (int e = 0; e < CH; ++e) {
               const float x = fmaf(ptx::sqrt_approx(v[e]), inv_h_s, 1.f / kSScale);

@@ -48,6 +48,24 @@ __device__ __forceinline__ double gauss_at(unsigned long long seed, long long i)
   return (i & 1) ? r * sin(th) : r * cos(th);
 }
 
+// Both Gaussians of Box-Muller pair p (numbers 2p and 2p + 1): one log, one
+// sqrt and one sincos for two samples.
+__device__ __forceinline__ void gauss_pair(unsigned long long seed, unsigned long long p, double& g_even,
+                                           double& g_odd) {
+  const unsigned long long d1 = seed + (2 * p + 1) * 0x9e3779b97f4a7c15ULL;
+  const unsigned long long d2 = seed + (2 * p + 2) * 0x9e3779b97f4a7c15ULL;
+  const unsigned long long z1 = sm64_mix(d1 - 0x9e3779b97f4a7c15ULL);
+  const unsigned long long z2 = sm64_mix(d2 - 0x9e3779b97f4a7c15ULL);
+  const double u1 = (static_cast<double>(z1 >> 11) + 1.0) * 0x1.0p-53;
+  const double u2 = static_cast<double>(z2 >> 11) * 0x1.0p-53;
+  const double r = sqrt(-2.0 * log(u1));
+  const double th = 2.0 * 3.14159265358979323846 * u2;
+  double sn, cs;
+  sincos(th, &sn, &cs);
+  g_even = r * cs;
+  g_odd = r * sn;
+}
+
 // per-channel stream seeds derive_seed(seed, {s}) (rng.hpp:26-33)
 __global__ void synth_seeds_kernel(unsigned long long seed, int n, unsigned long long* seeds) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -77,9 +95,23 @@ __global__ void synth_ar_local_kernel(const unsigned long long* seeds, int n, in
   const int s = static_cast<int>(id / chunks);
   const int64_t c = id % chunks;
   const int64_t t0 = c * kChunkT, t1 = min(N, t0 + kChunkT);
+  const unsigned long long seed = seeds[s];
   double st = 0.0;
+  double held = 0.0;  // odd member of the current pair
   for (int64_t t = t0; t < t1; ++t) {
-    st = phi * st + gauss_at(seeds[s], kBurnIn + 1 + t);
+    const long long i = kBurnIn + 1 + t;
+    double g;
+    if (i & 1) {
+      if (t == t0) {
+        double ge;
+        gauss_pair(seed, static_cast<unsigned long long>(i >> 1), ge, g);
+      } else {
+        g = held;
+      }
+    } else {
+      gauss_pair(seed, static_cast<unsigned long long>(i >> 1), g, held);
+    }
+    st = phi * st + g;
     out[t + s * N] = st;
   }
   chunk_end[id] = st;
@@ -101,14 +133,22 @@ __global__ void synth_ar_carry_kernel(const double* state0, const double* chunk_
   }
 }
 
-__global__ void synth_ar_apply_kernel(const double* carry, int n, int64_t N, double phi, double* out) {
+// phi^(i + 1) for i < kChunkT (the same pow values the apply pass used to
+// compute per element: an FP64 pow per sample made that pass compute-bound)
+__global__ void synth_phi_pow_kernel(double phi, double* phipow) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < kChunkT) phipow[i] = pow(phi, static_cast<double>(i + 1));
+}
+
+__global__ void synth_ar_apply_kernel(const double* carry, const double* __restrict__ phipow, int n, int64_t N,
+                                      double* out) {
   const int64_t total = static_cast<int64_t>(n) * N;
   const int64_t chunks = (N + kChunkT - 1) / kChunkT;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = e / N, t = e % N;
     const int64_t c = t / kChunkT, i = t % kChunkT;
-    out[e] += pow(phi, static_cast<double>(i + 1)) * carry[s * chunks + c];
+    out[e] += phipow[i] * carry[s * chunks + c];
   }
 }
 
@@ -145,10 +185,12 @@ __global__ void __launch_bounds__(256) col_moments_kernel(const double* X, int64
   }
 }
 
-// standardise (signals.cpp:224-227) and mix with the compound-symmetric
-// Cholesky factor: diag[s] = L(s,s), below[k] = L(j,k) for j > k.
+// standardise (signals.cpp:224-227), mix with the compound-symmetric
+// Cholesky factor (diag[s] = L(s,s), below[k] = L(j,k) for j > k) and apply
+// the Fleishman cubic (signals.cpp:241-248) in the same pass.
 __global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* mean, const double* sd,
-                                     const double* diag, const double* below, int mix) {
+                                     const double* diag, const double* below, int mix, double fa, double fb,
+                                     double fc, double fd) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= N) return;
   double acc = 0.0;
@@ -156,31 +198,27 @@ __global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* 
     double v = X[t + s * N];
     const double d = sd[s] > 0.0 ? sd[s] : 1.0;
     v = (v - mean[s]) / d;
+    double o = v;
     if (mix) {
-      const double o = diag[s] * v + acc;
+      o = diag[s] * v + acc;
       acc += below[s] * v;
-      X[t + s * N] = o;
-    } else {
-      X[t + s * N] = v;
     }
+    X[t + s * N] = fa + o * (fb + o * (fc + o * fd));
   }
 }
 
-__global__ void synth_cubic_kernel(double* X, int64_t total, double a, double b, double c, double d) {
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double v = X[e];
-    X[e] = a + v * (b + v * (c + v * d));
-  }
+// per-channel variance factor sqrt(variance) / sd (signals.cpp:249-251),
+// formed once per channel instead of per element
+__global__ void synth_scale_factor_kernel(const double* sd, int n, double variance, double* f) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) f[s] = sqrt(variance) / (sd[s] > 0.0 ? sd[s] : 1.0);
 }
 
-__global__ void synth_scale_kernel(double* X, int n, int64_t N, const double* sd, double variance) {
+__global__ void synth_scale_kernel(double* X, int n, int64_t N, const double* __restrict__ f) {
   const int64_t total = static_cast<int64_t>(n) * N;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double s = sd[e / N] > 0.0 ? sd[e / N] : 1.0;
-    X[e] *= sqrt(variance) / s;
-  }
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    X[e] *= f[e / N];
 }
 
 }  // namespace csb

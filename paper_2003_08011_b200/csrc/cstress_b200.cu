@@ -741,7 +741,7 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
       if (it == fit.end()) {
         cudaLaunchConfig_t q{};
         q.gridDim = dim3(static_cast<unsigned>(ctx->sm_count / cl * cl));
-        q.blockDim = dim3(kTcThreads);
+        q.blockDim = dim3(tc_threads(M->NB, M->SB));
         q.dynamicSmemBytes = smem;
         cudaLaunchAttribute a{};
         a.id = cudaLaunchAttributeClusterDimension;
@@ -768,7 +768,7 @@ void launch_tc(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* obs, i
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(g));
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(tc_threads(M->NB, M->SB));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr{};

@@ -16,7 +16,7 @@
 //                n_stages-deep shared-memory rings
 //   warps 2, 3   MMA issuers (one thread each): tcgen05.mma kind::f16, GEMM1
 //                (warp 2) one or two steps ahead of GEMM2 (warp 3).
-//   warps 4..19  epilogue: two sets of 8 warps; set e owns the steps with
+//   warps 4..    epilogue (16, or 8, see tc_epi_warps): two sets; set e owns the steps with
 //                j % 2 == e (and TMEM buffer e), each warp a 32-lane quarter
 //                and half of the MT columns.  All 16 warps share the x
 //                prologue and the final estimate / residual readout.
@@ -44,9 +44,23 @@
 
 namespace csb {
 
-constexpr int kEpiWarps = 16;
-constexpr int kEpiThreads = 32 * kEpiWarps;         // 512
-constexpr int kTcThreads = 128 + kEpiThreads;       // 640: 2 producers, 2 MMA issuers, epilogue
+// Epilogue warps per TMEM plan: 16 (two sets of 8 with NB = 2), or 8 for
+// double-ACC single-S plans (sets of 4, each warp a whole step's columns for
+// its lane quarter).  8 leave 168 registers per thread instead of 96 (the
+// register file is split over the four SMSPs, and 20 warps put five on one
+// of them); measured: 12% faster with (64,2,1) at n = 128, 9% slower with
+// (64,2,2) at C2 (fewer warps to hide the kernel map's latency).
+// CSB_EPI_WARPS=8|16 forces one count for every plan (A/B builds).
+__host__ __device__ constexpr int tc_epi_warps(int NB, int SB) {
+#ifdef CSB_EPI_WARPS
+  return CSB_EPI_WARPS + 0 * (NB + SB);
+#else
+  return (NB == 2 && SB == 1) ? 8 : 16;
+#endif
+}
+__host__ __device__ constexpr int tc_threads(int NB, int SB) {
+  return 128 + 32 * tc_epi_warps(NB, SB);  // 2 producers, 2 MMA issuers, epilogue
+}
 constexpr int kObsTile = 128;
 constexpr int kTmemCols = 512;
 constexpr int kMaxStages = 4;
@@ -158,7 +172,7 @@ struct Ring {
 //         similarity epilogue).  NB = 1: single buffers, all 16 epilogue
 //         warps work on every step (4 column groups), GEMM1 one step ahead.
 template <int MT, int NB, int SB, typename IO, bool STAGED>
-__global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(tc_threads(NB, SB), 1) mset_estimate_tc_kernel(const __grid_constant__ TcParams p) {
   static_assert(NB == 1 || NB == 2, "one or two TMEM buffers");
   static_assert(SB >= 1 && SB <= NB, "S buffers");
   static_assert(!STAGED || sizeof(IO) == 4, "staged tile edge: FP32 I/O");
@@ -166,8 +180,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
   // sets -- the set that does not own the last step stages the next tile's x
   // (it is done with the tile first), the other reads O out; see the epilogue.
   const bool kSplitEdge = STAGED && NB == 2 && p.split_edge;
+  constexpr int kEpiWarps = tc_epi_warps(NB, SB);
+  static_assert(kEpiWarps == 8 || kEpiWarps == 16, "8 or 16 epilogue warps");
   constexpr int kSetWarps = kEpiWarps / NB;      // warps per step set
-  constexpr int COLS = MT * NB / 4;              // columns per epilogue warp
+  constexpr int COLS = MT * 4 / kSetWarps;       // columns per epilogue warp
   constexpr int CH = COLS % 16 == 0 ? 16 : 8;    // TMEM access chunk
   static_assert(COLS % 8 == 0, "epilogue column slice must be a multiple of 8");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -445,11 +461,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;               // 0..15 (warps 4..19: every lane quarter
+    const int ew = warp - 4;               // 0..kEpiWarps-1 (every lane quarter
                                            // appears once in each group of four)
     const int q = warp & 3;                // TMEM lane quarter this warp may access
-    const int set = NB == 2 ? (ew >> 3) : 0;                // step parity owned
-    const int half = NB == 2 ? ((ew >> 2) & 1) : (ew >> 2);  // column slice in step
+    const int set = NB == 2 ? ew / kSetWarps : 0;  // step parity owned
+    const int half = (ew % kSetWarps) >> 2;        // column slice in step
+    const bool tl_lead = ew % kSetWarps == 0;      // timeline recorder of the set (CSB_TIMELINE)
+    const int tl_slot = 2 + ew / kSetWarps;
+    (void)tl_lead;
+    (void)tl_slot;
     // Tile edge (x prologue of the next tile, O readout of this one).  Split
     // edge: the set that does not own step T-1 runs the prologue (8 warps)
     // while the owner of T-1 finishes it and reads O out (8 warps); the
@@ -534,7 +554,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
     constexpr int PB = sizeof(IO) == 8 ? 2 : 4;  // chunks per load batch
     const uint32_t w_xx = static_cast<uint32_t>(p.n + 1) / 2;  // f16x2 word holding column n + 1
     auto prologue = [&](int tile, bool& bad_row) -> float {
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 20, tile);
+      if (tl_lead) CSB_TL(tl_slot, 20, tile);
       const int64_t t = static_cast<int64_t>(tile) * kObsTile + row;
       const bool valid = t < p.N;
       float acc = 0.f;
@@ -544,7 +564,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       const float* xs = nullptr;
       if constexpr (STAGED) {
         wait(xa_full, kt & 1);
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 45, tile);
+        if (tl_lead) CSB_TL(tl_slot, 45, tile);
         xs = s_stage;
       }
       // split and store one normalised 8-column chunk of the operand
@@ -570,7 +590,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         ++prologue_count;
         ptx::tc_fence_after();
         waited = true;
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 21, tile);
+        if (tl_lead) CSB_TL(tl_slot, 21, tile);
         for (int k8 = gi; k8 < K1 / 8; k8 += kBG) {
           float xv[8];
           const int c = min(k8, (p.n - 1) / 8);
@@ -597,7 +617,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             wait(x_free, (prologue_count & 1) ^ 1);
             ++prologue_count;
             ptx::tc_fence_after();
-            if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 21, tile);
+            if (tl_lead) CSB_TL(tl_slot, 21, tile);
             waited = true;
           }
 #pragma unroll
@@ -613,13 +633,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
         ptx::tc_fence_after();
       }
       const int par = kt & 1;
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 42, tile);
+      if (tl_lead) CSB_TL(tl_slot, 42, tile);
       float* xx_part = s_xx + par * 4 * kObsTile;
       uint8_t* bad_part = s_bad + par * 4 * kObsTile;
       xx_part[gi * kObsTile + row] = acc;
       bad_part[gi * kObsTile + row] = bad && valid;
       ptx::named_bar_sync(1, kBW * 32);
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 43, tile);
+      if (tl_lead) CSB_TL(tl_slot, 43, tile);
       float xx = 0.f;
 #pragma unroll
       for (int g = 0; g < kBG; ++g) {
@@ -651,7 +671,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       ptx::tc_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 22, tile);
+      if (tl_lead) CSB_TL(tl_slot, 22, tile);
       if (lane == 0) ptx::mbar_arrive(x_ready);
       bad_row = bad;
       return xx;
@@ -765,10 +785,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             ptx::tmem_st4(tmem + lane_off + s_base + MT / 2 + (c * CH + h8 * 8) / 2, lo);
           }
         };
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 10, j);
+        if (tl_lead) CSB_TL(tl_slot, 10, j);
         wait(&acc_full[set], use & 1);
         ptx::tc_fence_after();
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 11, j);
+        if (tl_lead) CSB_TL(tl_slot, 11, j);
         if constexpr (SB == 1) {
           // single S buffer: release ACC as early as possible (GEMM1 of the
           // next step may start), then wait for GEMM2 of the previous step
@@ -784,7 +804,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           if (lane == 0) ptx::mbar_arrive(&acc_free[set]);  // GEMM1 may refill ACC now
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
-          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
+          if (tl_lead) CSB_TL(tl_slot, 12, j);
           if constexpr (NB == 1) {
             wait(&s_free[0], (use & 1) ^ 1);
           } else if (tcount != 0 || j != 0) {  // the CTA's first step has no predecessor
@@ -792,7 +812,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             ++s_waits;
           }
           ptx::tc_fence_after();
-          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 13, j);
+          if (tl_lead) CSB_TL(tl_slot, 13, j);
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) store_chunk(c, vall + c * CH);
         } else {
@@ -800,24 +820,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           // two steps ahead overlaps the kernel map), then map and store S
           float vall[COLS];
           load_acc(vall);
-          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 46, j);
+          if (tl_lead) CSB_TL(tl_slot, 46, j);
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&acc_free[set]);
           // map first, then wait for GEMM2(j - 2) to have read S[set]
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) compute_chunk(c, vall + c * CH);
-          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 12, j);
+          if (tl_lead) CSB_TL(tl_slot, 12, j);
           wait(&s_free[set], (use & 1) ^ 1);
           ptx::tc_fence_after();
-          if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 13, j);
+          if (tl_lead) CSB_TL(tl_slot, 13, j);
 #pragma unroll
           for (int c = 0; c < COLS / CH; ++c) store_chunk(c, vall + c * CH);
         }
         ptx::tc_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 14, j);
+        if (tl_lead) CSB_TL(tl_slot, 14, j);
         if (lane == 0) ptx::mbar_arrive(&s_ready[sbuf]);
         if (x_due) {  // staged issuer, first step of the tile: stage x(k + 1) and x(k)
           ptx::bulk_wait_read0();  // the previous edge's stores have read both halves
@@ -837,7 +857,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
       // observations of a batch are loaded before waiting for O.
       const bool issuer = issuer_thread;
       if (do_read) {
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 23, tile);
+        if (tl_lead) CSB_TL(tl_slot, 23, tile);
         float* s_out = s_stage;  // est -> half A, resid -> half B (over x)
         bool o_ready = false;
         if constexpr (STAGED) {
@@ -849,7 +869,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             if (kSplitEdge && next < tile_end) wait(a_done, (tcount + 1) & 1);
             wait(o_full, tcount & 1);
             ptx::tc_fence_after();
-            if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
+            if (tl_lead) CSB_TL(tl_slot, 24, tile);
             o_ready = true;
             // O read CSB_RD_BATCH chunks per TMEM wait
             constexpr int OB = CSB_RD_BATCH;
@@ -859,7 +879,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
               for (int b = 0; b < OB; ++b)
                 if (c0 + b * kBG < N2 / 8) ptx::tmem_ld8(tmem + lane_off + colO + (c0 + b * kBG) * 8, o[b]);
               ptx::tc_wait_ld();
-              if ((ew & 7) == 0 && c0 == gi) CSB_TL(2 + (ew >> 3), 44, tile);
+              if (tl_lead && c0 == gi) CSB_TL(tl_slot, 44, tile);
 #pragma unroll
               for (int b = 0; b < OB; ++b) {
                 const int c = c0 + b * kBG;
@@ -888,7 +908,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             if (!o_ready) {
               wait(o_full, tcount & 1);
               ptx::tc_fence_after();
-              if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 24, tile);
+              if (tl_lead) CSB_TL(tl_slot, 24, tile);
               o_ready = true;
             }
 #pragma unroll
@@ -897,7 +917,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
               if (c >= N2 / 8) break;
               float o[8];
               ptx::tmem_ld8_wait(tmem + lane_off + colO + c * 8, o);
-              if ((ew & 7) == 0 && c == gi) CSB_TL(2 + (ew >> 3), 44, tile);
+              if (tl_lead && c == gi) CSB_TL(tl_slot, 44, tile);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const int s = c * 8 + e;
@@ -920,7 +940,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           wait(o_full, tcount & 1);
           ptx::tc_fence_after();
         }
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 27, tile);
+        if (tl_lead) CSB_TL(tl_slot, 27, tile);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(o_free);  // O read: the next tile's GEMM2 may start
@@ -934,7 +954,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
             ptx::bulk_commit();
           }
         }
-        if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 25, tile);
+        if (tl_lead) CSB_TL(tl_slot, 25, tile);
       }
       if (next < tile_end) {
         if (do_pro) {
@@ -945,7 +965,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mset_estimate_tc_kernel(const _
           fetch_xx(tcount + 1);
         }
       }
-      if ((ew & 7) == 0) CSB_TL(2 + (ew >> 3), 26, tile);
+      if (tl_lead) CSB_TL(tl_slot, 26, tile);
     }
     if (STAGED && issuer_thread) ptx::bulk_wait0();  // stores complete before exit
   }

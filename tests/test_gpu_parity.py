@@ -437,3 +437,32 @@ def test_fused_many_tiles_per_cta(p, oracle, shape, n, m):
     sel = np.arange(0, N, 997)
     o = oracle.train(X, m, 0)
     assert rel(r.estimates[sel], oracle.estimate(o, obs[sel])[0]) <= FP32_TOL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("cluster", ["2", "4"])
+def test_fused_cluster_multicast(p, oracle, cluster):
+    """CSB_CLUSTER=2|4: CTA clusters share the D_norm / P operand stream by
+    multicast bulk copies (each CTA loads a 1/CL slice into every CTA of the
+    cluster; slots freed by multicast MMA commits).  Same results as the
+    plain launch, including dummy tile slots when the tile count is not a
+    multiple of the cluster size."""
+    import os
+    import torch
+    n, m, N = 100, 1000, 128 * (148 * 2 + 3) + 11
+    X = oracle.synthesize_uniform(n, 4 * m, 0.5, 0.3, 1.0, 0.5, 4.0, 51)
+    obs = oracle.synthesize_uniform(n, N, 0.5, 0.3, 1.0, 0.5, 4.0, 53)
+    g = p.train(X, m, p.KernelConfig(), B(p, "fp32"))
+    d_obs = torch.tensor(obs.T.astype(np.float32), device="cuda").T
+    out = {}
+    for cl in ("1", cluster):
+        os.environ["CSB_CLUSTER"] = cl
+        try:
+            e = torch.full_like(d_obs.T, float("nan")).T
+            r = torch.full_like(d_obs.T, float("nan")).T
+            p.estimate_device(g, d_obs, e, r)
+            torch.cuda.synchronize()
+            out[cl] = (e.cpu().numpy(), r.cpu().numpy())
+        finally:
+            del os.environ["CSB_CLUSTER"]
+    assert np.array_equal(out["1"][0], out[cluster][0]) and np.array_equal(out["1"][1], out[cluster][1])

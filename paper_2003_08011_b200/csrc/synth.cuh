@@ -32,22 +32,6 @@ __device__ __forceinline__ unsigned long long sm64_mix(unsigned long long z) {
   return z ^ (z >> 31);
 }
 
-// Gaussian number i (0-based) of the stream seeded with `seed`.
-__device__ __forceinline__ double gauss_at(unsigned long long seed, long long i) {
-  const unsigned long long p = static_cast<unsigned long long>(i >> 1);
-  const unsigned long long d1 = seed + (2 * p + 1) * 0x9e3779b97f4a7c15ULL;
-  const unsigned long long d2 = seed + (2 * p + 2) * 0x9e3779b97f4a7c15ULL;
-  // next_u64 increments the state before mixing: draw k uses state seed + k*gamma,
-  // and mix() adds gamma once more -> pass state - gamma.
-  const unsigned long long z1 = sm64_mix(d1 - 0x9e3779b97f4a7c15ULL);
-  const unsigned long long z2 = sm64_mix(d2 - 0x9e3779b97f4a7c15ULL);
-  const double u1 = (static_cast<double>(z1 >> 11) + 1.0) * 0x1.0p-53;
-  const double u2 = static_cast<double>(z2 >> 11) * 0x1.0p-53;
-  const double r = sqrt(-2.0 * log(u1));
-  const double th = 2.0 * 3.14159265358979323846 * u2;
-  return (i & 1) ? r * sin(th) : r * cos(th);
-}
-
 // Both Gaussians of Box-Muller pair p (numbers 2p and 2p + 1): one log, one
 // sqrt and one sincos for two samples.
 __device__ __forceinline__ void gauss_pair(unsigned long long seed, unsigned long long p, double& g_even,
@@ -81,40 +65,76 @@ __global__ void synth_burnin_kernel(const unsigned long long* seeds, int n, doub
                                     double* state0) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
-  double st = gauss_at(seeds[s], 0);
-  for (int t = 1; t <= kBurnIn; ++t) st = phi * st + gauss_at(seeds[s], t);
+  // Gaussians 0..kBurnIn in Box-Muller pairs (one log/sqrt/sincos per two)
+  const unsigned long long seed = seeds[s];
+  double ge, go;
+  gauss_pair(seed, 0, ge, go);
+  double st = phi * ge + go;
+  for (int p = 1; 2 * p <= kBurnIn; ++p) {
+    gauss_pair(seed, static_cast<unsigned long long>(p), ge, go);
+    st = phi * st + ge;
+    if (2 * p + 1 <= kBurnIn) st = phi * st + go;
+  }
   state0[s] = st;
 }
 
-// local recurrences from a zero state; thread = (channel, chunk)
-__global__ void synth_ar_local_kernel(const unsigned long long* seeds, int n, int64_t N, double phi,
-                                      double* out, double* chunk_end) {
+// local recurrences from a zero state; thread = (channel, chunk).  A lane
+// owns one chunk, so its own time steps are 8 KB apart from its neighbours':
+// the values go through a per-warp 32 x 32 shared-memory transpose and leave
+// as one coalesced 256-byte row per chunk (direct per-lane stores wrote one
+// 8-byte word per 32-byte sector, 13 GB of DRAM writes for 8 GB of output).
+constexpr int kArThreads = 128;
+__global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsigned long long* seeds, int n,
+                                                                    int64_t N, double phi, double* out,
+                                                                    double* chunk_end) {
+  __shared__ double tile[kArThreads / 32][32][33];
   const int64_t chunks = (N + kChunkT - 1) / kChunkT;
-  const int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (id >= chunks * n) return;
-  const int s = static_cast<int>(id / chunks);
-  const int64_t c = id % chunks;
-  const int64_t t0 = c * kChunkT, t1 = min(N, t0 + kChunkT);
-  const unsigned long long seed = seeds[s];
+  const int64_t total = chunks * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t warp0 = blockIdx.x * static_cast<int64_t>(kArThreads) + warp * 32;
+  if (warp0 >= total) return;  // whole warp idle
+  const int64_t id = warp0 + lane;
+  const bool active = id < total;
+  const int s = active ? static_cast<int>(id / chunks) : 0;
+  const int64_t c = active ? id % chunks : 0;
+  const int64_t t0 = c * kChunkT;
+  const int len = active ? static_cast<int>(min(static_cast<int64_t>(kChunkT), N - t0)) : 0;
+  const unsigned long long seed = active ? seeds[s] : 0ULL;
+  const long long base = static_cast<long long>(s) * N + t0;  // out offset of this lane's chunk
+  double (*sm)[33] = tile[warp];
   double st = 0.0;
   double held = 0.0;  // odd member of the current pair
-  for (int64_t t = t0; t < t1; ++t) {
-    const long long i = kBurnIn + 1 + t;
-    double g;
-    if (i & 1) {
-      if (t == t0) {
-        double ge;
-        gauss_pair(seed, static_cast<unsigned long long>(i >> 1), ge, g);
-      } else {
-        g = held;
+  for (int k = 0; k < kChunkT; k += 32) {
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+      const int tt = k + j;
+      if (tt < len) {
+        const long long i = kBurnIn + 1 + t0 + tt;
+        double g;
+        if (i & 1) {
+          if (tt == 0) {
+            double ge;
+            gauss_pair(seed, static_cast<unsigned long long>(i >> 1), ge, g);
+          } else {
+            g = held;
+          }
+        } else {
+          gauss_pair(seed, static_cast<unsigned long long>(i >> 1), g, held);
+        }
+        st = phi * st + g;
       }
-    } else {
-      gauss_pair(seed, static_cast<unsigned long long>(i >> 1), g, held);
+      sm[lane][j] = st;
     }
-    st = phi * st + g;
-    out[t + s * N] = st;
+    __syncwarp();
+    // row r = chunk of lane r: 32 consecutive time steps, one per lane
+    for (int r = 0; r < 32; ++r) {
+      const long long br = __shfl_sync(0xffffffffu, base, r);
+      const int lr = __shfl_sync(0xffffffffu, len, r);
+      if (k + lane < lr) out[br + k + lane] = sm[r][lane];
+    }
+    __syncwarp();
   }
-  chunk_end[id] = st;
+  if (active) chunk_end[id] = st;
 }
 
 // carry into each chunk (sequential over chunks, one thread per channel)
@@ -140,71 +160,141 @@ __global__ void synth_phi_pow_kernel(double phi, double* phipow) {
   if (i < kChunkT) phipow[i] = pow(phi, static_cast<double>(i + 1));
 }
 
-__global__ void synth_ar_apply_kernel(const double* carry, const double* __restrict__ phipow, int n, int64_t N,
-                                      double* out) {
-  const int64_t total = static_cast<int64_t>(n) * N;
+// out += phi^(i+1) * carry, fused with the per-channel moments of the AR
+// streams: block (t-range of kApplyT samples, channel) writes the shifted sums
+// (sum d, sum d^2), d = x - K with K = the channel's burn-in state (a
+// read-only value on the data's scale, same for every block).
+constexpr int kApplyT = 2048;
+__global__ void __launch_bounds__(256) synth_ar_apply_kernel(const double* carry, const double* __restrict__ phipow,
+                                                             int64_t N, double* out, double2* part) {
+  __shared__ double red[2][8];
+  const int64_t s = blockIdx.y;
   const int64_t chunks = (N + kChunkT - 1) / kChunkT;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = e / N, t = e % N;
-    const int64_t c = t / kChunkT, i = t % kChunkT;
-    out[e] += phipow[i] * carry[s * chunks + c];
+  const double K = carry[s * chunks];
+  double* col = out + s * N;
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int k = 0; k < kApplyT / 256; ++k) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kApplyT + k * 256 + threadIdx.x;
+    if (t < N) {
+      const double v = col[t] + phipow[t % kChunkT] * carry[s * chunks + t / kChunkT];
+      col[t] = v;
+      const double d = v - K;
+      a += d;
+      b += d * d;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      A += red[0][w];
+      B += red[1][w];
+    }
+    part[s * gridDim.x + blockIdx.x] = make_double2(A, B);
   }
 }
 
-// per-column mean and population std (block per column, tree reduction)
+// mean and 1 / population std per channel from the apply pass's block sums
+__global__ void synth_ar_moments_kernel(const double* carry, const double2* __restrict__ part, int n, int64_t N,
+                                        int nb, double* mean, double* isd) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+  double A = 0.0, B = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    const double2 v = part[static_cast<int64_t>(s) * nb + i];
+    A += v.x;
+    B += v.y;
+  }
+  const double Nd = static_cast<double>(N), md = A / Nd;
+  mean[s] = carry[s * chunks] + md;
+  const double d = sqrt(fmax(B / Nd - md * md, 0.0));
+  isd[s] = 1.0 / (d > 0.0 ? d : 1.0);  // N == 1 degenerate stream (signals.cpp:226)
+}
+
+// per-column mean and population std in one pass (block per column): sums
+// of d = x - x_0 and d^2, shifted by the column's first value so the
+// E[d^2] - E[d]^2 form does not cancel; exactly 0 for a constant column.
 __global__ void __launch_bounds__(256) col_moments_kernel(const double* X, int64_t N, double* mean,
                                                           double* sd) {
-  __shared__ double red[256];
+  __shared__ double red[2][8];
   const int64_t s = blockIdx.x;
   const double* col = X + s * N;
-  double a = 0.0;
-  for (int64_t t = threadIdx.x; t < N; t += blockDim.x) a += col[t];
-  red[threadIdx.x] = a;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
+  const double K = col[0];
+  double a = 0.0, b = 0.0;
+  int64_t t = threadIdx.x;
+  for (; t + 3 * 256 < N; t += 4 * 256) {
+    const double d0 = col[t] - K, d1 = col[t + 256] - K, d2 = col[t + 512] - K, d3 = col[t + 768] - K;
+    a += (d0 + d1) + (d2 + d3);
+    b += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
   }
-  const double mu = red[0] / static_cast<double>(N);
-  __syncthreads();
-  double b = 0.0;
-  for (int64_t t = threadIdx.x; t < N; t += blockDim.x) {
-    const double d = col[t] - mu;
+  for (; t < N; t += 256) {
+    const double d = col[t] - K;
+    a += d;
     b += d * d;
   }
-  red[threadIdx.x] = b;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
   }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    mean[s] = mu;
-    sd[s] = sqrt(red[0] / static_cast<double>(N));
+    double A = 0.0, B = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      A += red[0][w];
+      B += red[1][w];
+    }
+    const double Nd = static_cast<double>(N);
+    const double md = A / Nd;
+    mean[s] = K + md;
+    sd[s] = sqrt(fmax(B / Nd - md * md, 0.0));
   }
 }
 
-// standardise (signals.cpp:224-227), mix with the compound-symmetric
-// Cholesky factor (diag[s] = L(s,s), below[k] = L(j,k) for j > k) and apply
-// the Fleishman cubic (signals.cpp:241-248) in the same pass.
-__global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* mean, const double* sd,
-                                     const double* diag, const double* below, int mix, double fa, double fb,
-                                     double fc, double fd) {
+// standardise (signals.cpp:224-227; multiply by the channel's 1/sd), mix
+// with the compound-symmetric Cholesky factor (diag[s] = L(s,s), below[k] =
+// L(j,k) for j > k) and apply the Fleishman cubic (signals.cpp:241-248) in the
+// same pass.  Thread per time step, channels in groups of four loaded ahead
+// of the dependent running sum.
+__global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* __restrict__ mean,
+                                     const double* __restrict__ isd, const double* __restrict__ diag,
+                                     const double* __restrict__ below, int mix, double fa, double fb, double fc,
+                                     double fd) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= N) return;
   double acc = 0.0;
-  for (int s = 0; s < n; ++s) {
-    double v = X[t + s * N];
-    const double d = sd[s] > 0.0 ? sd[s] : 1.0;
-    v = (v - mean[s]) / d;
+  double* x = X + t;
+  int s = 0;
+  auto one = [&](int c, double v) {
+    v = (v - mean[c]) * isd[c];
     double o = v;
     if (mix) {
-      o = diag[s] * v + acc;
-      acc += below[s] * v;
+      o = diag[c] * v + acc;
+      acc += below[c] * v;
     }
-    X[t + s * N] = fa + o * (fb + o * (fc + o * fd));
+    x[c * N] = fa + o * (fb + o * (fc + o * fd));
+  };
+  for (; s + 4 <= n; s += 4) {
+    const double v0 = x[s * N], v1 = x[(s + 1) * N], v2 = x[(s + 2) * N], v3 = x[(s + 3) * N];
+    one(s, v0);
+    one(s + 1, v1);
+    one(s + 2, v2);
+    one(s + 3, v3);
   }
+  for (; s < n; ++s) one(s, x[s * N]);
 }
 
 // per-channel variance factor sqrt(variance) / sd (signals.cpp:249-251),
@@ -214,11 +304,15 @@ __global__ void synth_scale_factor_kernel(const double* sd, int n, double varian
   if (s < n) f[s] = sqrt(variance) / (sd[s] > 0.0 ? sd[s] : 1.0);
 }
 
-__global__ void synth_scale_kernel(double* X, int n, int64_t N, const double* __restrict__ f) {
-  const int64_t total = static_cast<int64_t>(n) * N;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    X[e] *= f[e / N];
+// X(:, s) *= f[s]; block (t-range, channel), no per-element index division
+__global__ void synth_scale_kernel(double* X, int64_t N, const double* __restrict__ f) {
+  const double g = f[blockIdx.y];
+  double* col = X + static_cast<int64_t>(blockIdx.y) * N;
+#pragma unroll
+  for (int k = 0; k < kApplyT / 256; ++k) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kApplyT + k * 256 + threadIdx.x;
+    if (t < N) col[t] *= g;
+  }
 }
 
 }  // namespace csb

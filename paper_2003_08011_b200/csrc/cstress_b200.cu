@@ -1340,27 +1340,24 @@ cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double
     TmpBuf<unsigned long long> seeds(n);
     TmpBuf<double> state0(n), ends(n * chunks), carry(n * chunks), mean(n), sd(n), dg(n + 1), bl(n + 1),
         phipow(kChunkT), fscale(n), isd(n);
-    TmpBuf<double2> part(n * ceil_div(N, kApplyT));
+    TmpBuf<double> sums(3 * n * chunks);
+    const int nb = ceil_div(N, kApplyT);
     synth_seeds_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seed, static_cast<int>(n), seeds.get());
     synth_burnin_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), phi, state0.get());
-    synth_ar_local_kernel<<<ceil_div(n * chunks, kArThreads), kArThreads, 0, st>>>(
-        seeds.get(), static_cast<int>(n), N, phi, d_out, ends.get());
-    synth_ar_carry_kernel<<<ceil_div(n, 128), 128, 0, st>>>(state0.get(), ends.get(), static_cast<int>(n),
-                                                             N, phi, carry.get());
     synth_phi_pow_kernel<<<ceil_div(kChunkT, 256), 256, 0, st>>>(phi, phipow.get());
-    const int nb = ceil_div(N, kApplyT);
-    synth_ar_apply_kernel<<<dim3(nb, static_cast<unsigned>(n)), 256, 0, st>>>(carry.get(), phipow.get(), N,
-                                                                             d_out, part.get());
-    synth_ar_moments_kernel<<<ceil_div(n, 128), 128, 0, st>>>(carry.get(), part.get(), static_cast<int>(n), N,
-                                                              nb, mean.get(), isd.get());
+    synth_ar_local_kernel<<<ceil_div(n * chunks, kArThreads), kArThreads, 0, st>>>(
+        seeds.get(), static_cast<int>(n), N, phi, phipow.get(), d_out, ends.get(), sums.get());
+    synth_ar_carry_kernel<<<ceil_div(n, kCarryThreads / 32), kCarryThreads, 0, st>>>(
+        state0.get(), ends.get(), sums.get(), phipow.get(), static_cast<int>(n), N, phi, carry.get(), mean.get(),
+        isd.get());
     CSB_LAUNCH_CHECK();
     if (mix) {
       CSB_CUDA(cudaMemcpyAsync(dg.get(), diag.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
       CSB_CUDA(cudaMemcpyAsync(bl.get(), below.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
     }
-    synth_std_mix_kernel<<<ceil_div(N, 256), 256, 0, st>>>(d_out, static_cast<int>(n), N, mean.get(),
-                                                           isd.get(), dg.get(), bl.get(), mix ? 1 : 0, fc[0],
-                                                           fc[1], fc[2], fc[3]);
+    synth_std_mix_kernel<<<ceil_div(N, 256), 256, 0, st>>>(d_out, static_cast<int>(n), N, carry.get(),
+                                                           phipow.get(), mean.get(), isd.get(), dg.get(),
+                                                           bl.get(), mix ? 1 : 0, fc[0], fc[1], fc[2], fc[3]);
     col_moments_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_out, N, mean.get(), sd.get());
     synth_scale_factor_kernel<<<ceil_div(n, 128), 128, 0, st>>>(sd.get(), static_cast<int>(n), variance,
                                                                 fscale.get());

@@ -7,7 +7,9 @@
 //    even Gaussian, sin for the odd one, rng.hpp:162-176) is random-access.
 //  * AR(1) x_t = phi x_{t-1} + g_t is a linear recurrence: chunks of kChunkT
 //    samples run from a zero state in parallel, then chunk carries are chained
-//    (one thread per channel) and added back as phi^(i+1) * carry.
+//    (one thread per channel) and added back as phi^(i+1) * carry inside
+//    the standardise/mix pass; the channel moments come from per-chunk sums
+//    (no separate pass over the AR streams).
 //  * The mixing z L^T with the Cholesky factor of a compound-symmetric
 //    correlation matrix (unit diagonal, uniform rho) needs O(n) work per row:
 //    L(j,k) is the same value c_k for every j > k, so
@@ -43,9 +45,10 @@ __device__ __forceinline__ void gauss_pair(unsigned long long seed, unsigned lon
   const double u1 = (static_cast<double>(z1 >> 11) + 1.0) * 0x1.0p-53;
   const double u2 = static_cast<double>(z2 >> 11) * 0x1.0p-53;
   const double r = sqrt(-2.0 * log(u1));
-  const double th = 2.0 * 3.14159265358979323846 * u2;
+  // (sin, cos)(2 pi u2) as sincospi(2 u2): no argument reduction (2 u2 is
+  // exact); differs from the reference's rounded 2 pi u2 in the last ulp
   double sn, cs;
-  sincos(th, &sn, &cs);
+  sincospi(2.0 * u2, &sn, &cs);
   g_even = r * cs;
   g_odd = r * sn;
 }
@@ -85,8 +88,9 @@ __global__ void synth_burnin_kernel(const unsigned long long* seeds, int n, doub
 // 8-byte word per 32-byte sector, 13 GB of DRAM writes for 8 GB of output).
 constexpr int kArThreads = 128;
 __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsigned long long* seeds, int n,
-                                                                    int64_t N, double phi, double* out,
-                                                                    double* chunk_end) {
+                                                                    int64_t N, double phi,
+                                                                    const double* __restrict__ phipow, double* out,
+                                                                    double* chunk_end, double* chunk_sums) {
   __shared__ double tile[kArThreads / 32][32][33];
   const int64_t chunks = (N + kChunkT - 1) / kChunkT;
   const int64_t total = chunks * n;
@@ -104,6 +108,7 @@ __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsign
   double (*sm)[33] = tile[warp];
   double st = 0.0;
   double held = 0.0;  // odd member of the current pair
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0;  // sum l, sum l^2, sum l phi^(i+1)
   for (int k = 0; k < kChunkT; k += 32) {
 #pragma unroll 1
     for (int j = 0; j < 32; ++j) {
@@ -122,6 +127,9 @@ __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsign
           gauss_pair(seed, static_cast<unsigned long long>(i >> 1), g, held);
         }
         st = phi * st + g;
+        s1 += st;
+        s2 += st * st;
+        s3 += st * phipow[tt];
       }
       sm[lane][j] = st;
     }
@@ -134,22 +142,96 @@ __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsign
     }
     __syncwarp();
   }
-  if (active) chunk_end[id] = st;
+  if (active) {
+    chunk_end[id] = st;
+    chunk_sums[id] = s1;
+    chunk_sums[total + id] = s2;
+    chunk_sums[2 * total + id] = s3;
+  }
 }
 
-// carry into each chunk (sequential over chunks, one thread per channel)
-__global__ void synth_ar_carry_kernel(const double* state0, const double* chunk_end, int n, int64_t N,
-                                      double phi, double* carry) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
+// carry into each chunk and the channel's moments; one warp per channel.
+// The carry recurrence c_{k+1} = phi^len_k c_k + end_k is a chain of affine
+// maps: 32 chunks at a time go through a shuffle scan of map compositions,
+// chained block to block from the burn-in state.  The moments need no pass
+// over the data: with x_t = l_t + phi^(i+1) c (l the chunk-local stream, c the
+// chunk's carry, i the offset in the chunk), sum x = sum l + c G1 and sum x^2
+// = sum l^2 + 2 c sum l phi^(i+1) + c^2 G2, G1 = sum phi^(i+1), G2 = sum
+// phi^(2i+2) over the chunk.  Writes the mean and 1 / population std (floor
+// rule signals.cpp:226).
+constexpr int kCarryThreads = 128;
+__global__ void __launch_bounds__(kCarryThreads) synth_ar_carry_kernel(
+    const double* __restrict__ state0, const double* __restrict__ chunk_end, const double* __restrict__ chunk_sums,
+    const double* __restrict__ phipow, int n, int64_t N, double phi, double* __restrict__ carry,
+    double* __restrict__ mean, double* __restrict__ isd) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * (kCarryThreads / 32) + (threadIdx.x >> 5);
+  if (s >= n) return;  // warp-uniform
   const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+  const int64_t total = chunks * n;
+  double G1 = 0.0, G2 = 0.0;
+  for (int i = lane; i < kChunkT; i += 32) {
+    G1 += phipow[i];
+    G2 += phipow[i] * phipow[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    G1 += __shfl_xor_sync(0xffffffffu, G1, o);
+    G2 += __shfl_xor_sync(0xffffffffu, G2, o);
+  }
   const double phiC = pow(phi, static_cast<double>(kChunkT));
-  double cin = state0[s];  // state before the first chunk
-  for (int64_t c = 0; c < chunks; ++c) {
-    carry[s * chunks + c] = cin;
-    const int64_t len = min(static_cast<int64_t>(kChunkT), N - c * kChunkT);
-    const double pl = len == kChunkT ? phiC : pow(phi, static_cast<double>(len));
-    cin = pl * cin + chunk_end[s * chunks + c];
+  double x_in = state0[s];  // state before the current 32-chunk block
+  double A = 0.0, B = 0.0;
+  for (int64_t c0 = 0; c0 < chunks; c0 += 32) {
+    const int64_t c = c0 + lane;
+    const bool ok = c < chunks;
+    const int64_t id = s * chunks + c;
+    int64_t len = 0;
+    double a = 1.0, b = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, g1 = G1, g2 = G2;
+    if (ok) {
+      len = min(static_cast<int64_t>(kChunkT), N - c * kChunkT);
+      b = chunk_end[id];
+      s1 = chunk_sums[id];
+      s2 = chunk_sums[total + id];
+      s3 = chunk_sums[2 * total + id];
+      if (len == kChunkT) {
+        a = phiC;
+      } else {
+        a = pow(phi, static_cast<double>(len));
+        g1 = g2 = 0.0;
+        for (int i = 0; i < len; ++i) {
+          g1 += phipow[i];
+          g2 += phipow[i] * phipow[i];
+        }
+      }
+    }
+    // inclusive scan: (a, b) = f_lane o ... o f_0 of this block
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ap = __shfl_up_sync(0xffffffffu, a, o);
+      const double bp = __shfl_up_sync(0xffffffffu, b, o);
+      if (lane >= o) {
+        b = a * bp + b;
+        a = a * ap;
+      }
+    }
+    const double y = a * x_in + b;  // state after chunk `lane`
+    double cin = __shfl_up_sync(0xffffffffu, y, 1);
+    if (lane == 0) cin = x_in;
+    if (ok) {
+      carry[id] = cin;
+      A += s1 + cin * g1;
+      B += s2 + 2.0 * cin * s3 + cin * cin * g2;
+    }
+    x_in = __shfl_sync(0xffffffffu, y, 31);  // lanes past the end carry the identity map
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    A += __shfl_xor_sync(0xffffffffu, A, o);
+    B += __shfl_xor_sync(0xffffffffu, B, o);
+  }
+  if (lane == 0) {
+    const double Nd = static_cast<double>(N), mu = A / Nd;
+    mean[s] = mu;
+    const double d = sqrt(fmax(B / Nd - mu * mu, 0.0));
+    isd[s] = 1.0 / (d > 0.0 ? d : 1.0);
   }
 }
 
@@ -158,67 +240,6 @@ __global__ void synth_ar_carry_kernel(const double* state0, const double* chunk_
 __global__ void synth_phi_pow_kernel(double phi, double* phipow) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < kChunkT) phipow[i] = pow(phi, static_cast<double>(i + 1));
-}
-
-// out += phi^(i+1) * carry, fused with the per-channel moments of the AR
-// streams: block (t-range of kApplyT samples, channel) writes the shifted sums
-// (sum d, sum d^2), d = x - K with K = the channel's burn-in state (a
-// read-only value on the data's scale, same for every block).
-constexpr int kApplyT = 2048;
-__global__ void __launch_bounds__(256) synth_ar_apply_kernel(const double* carry, const double* __restrict__ phipow,
-                                                             int64_t N, double* out, double2* part) {
-  __shared__ double red[2][8];
-  const int64_t s = blockIdx.y;
-  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
-  const double K = carry[s * chunks];
-  double* col = out + s * N;
-  double a = 0.0, b = 0.0;
-#pragma unroll
-  for (int k = 0; k < kApplyT / 256; ++k) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * kApplyT + k * 256 + threadIdx.x;
-    if (t < N) {
-      const double v = col[t] + phipow[t % kChunkT] * carry[s * chunks + t / kChunkT];
-      col[t] = v;
-      const double d = v - K;
-      a += d;
-      b += d * d;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    red[0][threadIdx.x >> 5] = a;
-    red[1][threadIdx.x >> 5] = b;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double A = 0.0, B = 0.0;
-    for (int w = 0; w < 8; ++w) {
-      A += red[0][w];
-      B += red[1][w];
-    }
-    part[s * gridDim.x + blockIdx.x] = make_double2(A, B);
-  }
-}
-
-// mean and 1 / population std per channel from the apply pass's block sums
-__global__ void synth_ar_moments_kernel(const double* carry, const double2* __restrict__ part, int n, int64_t N,
-                                        int nb, double* mean, double* isd) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
-  double A = 0.0, B = 0.0;
-  for (int i = 0; i < nb; ++i) {
-    const double2 v = part[static_cast<int64_t>(s) * nb + i];
-    A += v.x;
-    B += v.y;
-  }
-  const double Nd = static_cast<double>(N), md = A / Nd;
-  mean[s] = carry[s * chunks] + md;
-  const double d = sqrt(fmax(B / Nd - md * md, 0.0));
-  isd[s] = 1.0 / (d > 0.0 ? d : 1.0);  // N == 1 degenerate stream (signals.cpp:226)
 }
 
 // per-column mean and population std in one pass (block per column): sums
@@ -264,21 +285,27 @@ __global__ void __launch_bounds__(256) col_moments_kernel(const double* X, int64
   }
 }
 
-// standardise (signals.cpp:224-227; multiply by the channel's 1/sd), mix
+// AR value = chunk-local value + phi^(i+1) carry, standardise
+// (signals.cpp:224-227; multiply by the channel's 1/sd), mix
 // with the compound-symmetric Cholesky factor (diag[s] = L(s,s), below[k] =
 // L(j,k) for j > k) and apply the Fleishman cubic (signals.cpp:241-248) in the
 // same pass.  Thread per time step, channels in groups of four loaded ahead
 // of the dependent running sum.
-__global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* __restrict__ mean,
+__global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* __restrict__ carry,
+                                     const double* __restrict__ phipow, const double* __restrict__ mean,
                                      const double* __restrict__ isd, const double* __restrict__ diag,
                                      const double* __restrict__ below, int mix, double fa, double fb, double fc,
                                      double fd) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= N) return;
+  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+  const double pw = phipow[t % kChunkT];
+  const double* cy = carry + t / kChunkT;
   double acc = 0.0;
   double* x = X + t;
   int s = 0;
   auto one = [&](int c, double v) {
+    v = v + pw * cy[c * chunks];  // chunk-local stream + phi^(i+1) carry = AR(1) value
     v = (v - mean[c]) * isd[c];
     double o = v;
     if (mix) {
@@ -305,6 +332,7 @@ __global__ void synth_scale_factor_kernel(const double* sd, int n, double varian
 }
 
 // X(:, s) *= f[s]; block (t-range, channel), no per-element index division
+constexpr int kApplyT = 2048;
 __global__ void synth_scale_kernel(double* X, int64_t N, const double* __restrict__ f) {
   const double g = f[blockIdx.y];
   double* col = X + static_cast<int64_t>(blockIdx.y) * N;

@@ -1335,7 +1335,18 @@ cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double
     const bool mix = n > 1;
     if (mix && !csb_uniform_cholesky(n, rho, diag, below))
       fail(CS_BAD_CORRELATION, "correlation matrix not positive semidefinite within jitter cap 1e-06");
-    const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+    // chunk length ct = 2^ct_log2 in [32, kChunkT]: the longest that still
+    // gives ~2 resident warps' worth of chunk walkers per SM, but no shorter
+    // than ~sqrt(N / 10), which balances a walker's ct sequential steps
+    // against the carry scan's N / (32 ct) dependent iterations per channel
+    // (both latency chains when n x N is small)
+    int occ_log2 = 10, lat_log2 = 5;
+    while (occ_log2 > 5 && n * ((N + (int64_t{1} << occ_log2) - 1) >> occ_log2) < int64_t{148} * 256 * 2)
+      --occ_log2;
+    while (lat_log2 < 10 && (int64_t{1} << (2 * (lat_log2 + 1))) * 10 <= N) ++lat_log2;
+    const int ct_log2 = std::max(occ_log2, lat_log2);
+    const int ct = 1 << ct_log2;
+    const int64_t chunks = (N + ct - 1) / ct;
     StreamScope scope(st);
     TmpBuf<unsigned long long> seeds(n);
     TmpBuf<double> state0(n), ends(n * chunks), carry(n * chunks), mean(n), sd(n), dg(n + 1), bl(n + 1),
@@ -1343,19 +1354,19 @@ cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double
     TmpBuf<double> sums(3 * n * chunks);
     const int nb = ceil_div(N, kApplyT);
     synth_seeds_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seed, static_cast<int>(n), seeds.get());
-    synth_burnin_kernel<<<ceil_div(n, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), phi, state0.get());
+    synth_burnin_kernel<<<ceil_div(n * 32, 128), 128, 0, st>>>(seeds.get(), static_cast<int>(n), phi, state0.get());
     synth_phi_pow_kernel<<<ceil_div(kChunkT, 256), 256, 0, st>>>(phi, phipow.get());
     synth_ar_local_kernel<<<ceil_div(n * chunks, kArThreads), kArThreads, 0, st>>>(
-        seeds.get(), static_cast<int>(n), N, phi, phipow.get(), d_out, ends.get(), sums.get());
+        seeds.get(), static_cast<int>(n), N, ct, phi, phipow.get(), d_out, ends.get(), sums.get());
     synth_ar_carry_kernel<<<ceil_div(n, kCarryThreads / 32), kCarryThreads, 0, st>>>(
-        state0.get(), ends.get(), sums.get(), phipow.get(), static_cast<int>(n), N, phi, carry.get(), mean.get(),
+        state0.get(), ends.get(), sums.get(), phipow.get(), static_cast<int>(n), N, ct, phi, carry.get(), mean.get(),
         isd.get());
     CSB_LAUNCH_CHECK();
     if (mix) {
       CSB_CUDA(cudaMemcpyAsync(dg.get(), diag.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
       CSB_CUDA(cudaMemcpyAsync(bl.get(), below.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
     }
-    synth_std_mix_kernel<<<ceil_div(N, 256), 256, 0, st>>>(d_out, static_cast<int>(n), N, carry.get(),
+    synth_std_mix_kernel<<<ceil_div(N, 256), 256, 0, st>>>(d_out, static_cast<int>(n), N, ct_log2, carry.get(),
                                                            phipow.get(), mean.get(), isd.get(), dg.get(),
                                                            bl.get(), mix ? 1 : 0, fc[0], fc[1], fc[2], fc[3]);
     col_moments_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_out, N, mean.get(), sd.get());

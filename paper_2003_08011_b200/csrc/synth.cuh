@@ -5,7 +5,7 @@
 //  * SplitMix64 is a counter generator: draw k of a channel stream is
 //    mix(seed_s + k*gamma), so Box-Muller pair p (draws 2p+1, 2p+2; cos for the
 //    even Gaussian, sin for the odd one, rng.hpp:162-176) is random-access.
-//  * AR(1) x_t = phi x_{t-1} + g_t is a linear recurrence: chunks of kChunkT
+//  * AR(1) x_t = phi x_{t-1} + g_t is a linear recurrence: chunks of ct
 //    samples run from a zero state in parallel, then chunk carries are chained
 //    (one thread per channel) and added back as phi^(i+1) * carry inside
 //    the standardise/mix pass; the channel moments come from per-chunk sums
@@ -24,7 +24,10 @@
 
 namespace csb {
 
-constexpr int kChunkT = 1024;
+constexpr int kChunkT = 1024;  // longest chunk (phi^(i+1) table size); the
+                               // runtime chunk length ct is a power of two in
+                               // [32, kChunkT], shorter when n x N is small so
+                               // the sequential chunk walks stay short
 constexpr int kBurnIn = 1000;  // signals.hpp:12
 
 __device__ __forceinline__ unsigned long long sm64_mix(unsigned long long z) {
@@ -62,23 +65,26 @@ __global__ void synth_seeds_kernel(unsigned long long seed, int n, unsigned long
   seeds[s] = h;
 }
 
-// burn-in state after g_0 and 1000 updates (signals.cpp:217-219), one thread
-// per channel.
-__global__ void synth_burnin_kernel(const unsigned long long* seeds, int n, double phi,
-                                    double* state0) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  // Gaussians 0..kBurnIn in Box-Muller pairs (one log/sqrt/sincos per two)
+// burn-in state after g_0 and 1000 updates (signals.cpp:217-219): state0 =
+// sum_t phi^(1000 - t) g_t, one warp per channel; lane L runs the recurrence
+// over t in [32 L, 32 L + 32) from zero (16 Box-Muller pairs) and the lanes'
+// partial states are combined with weights phi^(1000 - last t of the lane).
+__global__ void synth_burnin_kernel(const unsigned long long* seeds, int n, double phi, double* state0) {
+  const int lane = threadIdx.x & 31;
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n) return;  // warp-uniform
   const unsigned long long seed = seeds[s];
-  double ge, go;
-  gauss_pair(seed, 0, ge, go);
-  double st = phi * ge + go;
-  for (int p = 1; 2 * p <= kBurnIn; ++p) {
-    gauss_pair(seed, static_cast<unsigned long long>(p), ge, go);
+  const int t0 = 32 * lane, t1 = min(t0 + 31, kBurnIn);  // inclusive range
+  double st = 0.0;
+  for (int t = t0; t <= t1; t += 2) {
+    double ge, go;
+    gauss_pair(seed, static_cast<unsigned long long>(t >> 1), ge, go);
     st = phi * st + ge;
-    if (2 * p + 1 <= kBurnIn) st = phi * st + go;
+    if (t + 1 <= t1) st = phi * st + go;
   }
-  state0[s] = st;
+  double v = t0 <= t1 ? pow(phi, static_cast<double>(kBurnIn - t1)) * st : 0.0;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) state0[s] = v;
 }
 
 // local recurrences from a zero state; thread = (channel, chunk).  A lane
@@ -88,11 +94,11 @@ __global__ void synth_burnin_kernel(const unsigned long long* seeds, int n, doub
 // 8-byte word per 32-byte sector, 13 GB of DRAM writes for 8 GB of output).
 constexpr int kArThreads = 128;
 __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsigned long long* seeds, int n,
-                                                                    int64_t N, double phi,
+                                                                    int64_t N, int ct, double phi,
                                                                     const double* __restrict__ phipow, double* out,
                                                                     double* chunk_end, double* chunk_sums) {
   __shared__ double tile[kArThreads / 32][32][33];
-  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+  const int64_t chunks = (N + ct - 1) / ct;
   const int64_t total = chunks * n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t warp0 = blockIdx.x * static_cast<int64_t>(kArThreads) + warp * 32;
@@ -101,15 +107,15 @@ __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsign
   const bool active = id < total;
   const int s = active ? static_cast<int>(id / chunks) : 0;
   const int64_t c = active ? id % chunks : 0;
-  const int64_t t0 = c * kChunkT;
-  const int len = active ? static_cast<int>(min(static_cast<int64_t>(kChunkT), N - t0)) : 0;
+  const int64_t t0 = c * ct;
+  const int len = active ? static_cast<int>(min(static_cast<int64_t>(ct), N - t0)) : 0;
   const unsigned long long seed = active ? seeds[s] : 0ULL;
   const long long base = static_cast<long long>(s) * N + t0;  // out offset of this lane's chunk
   double (*sm)[33] = tile[warp];
   double st = 0.0;
   double held = 0.0;  // odd member of the current pair
   double s1 = 0.0, s2 = 0.0, s3 = 0.0;  // sum l, sum l^2, sum l phi^(i+1)
-  for (int k = 0; k < kChunkT; k += 32) {
+  for (int k = 0; k < ct; k += 32) {
 #pragma unroll 1
     for (int j = 0; j < 32; ++j) {
       const int tt = k + j;
@@ -162,15 +168,15 @@ __global__ void __launch_bounds__(kArThreads) synth_ar_local_kernel(const unsign
 constexpr int kCarryThreads = 128;
 __global__ void __launch_bounds__(kCarryThreads) synth_ar_carry_kernel(
     const double* __restrict__ state0, const double* __restrict__ chunk_end, const double* __restrict__ chunk_sums,
-    const double* __restrict__ phipow, int n, int64_t N, double phi, double* __restrict__ carry,
+    const double* __restrict__ phipow, int n, int64_t N, int ct, double phi, double* __restrict__ carry,
     double* __restrict__ mean, double* __restrict__ isd) {
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * (kCarryThreads / 32) + (threadIdx.x >> 5);
   if (s >= n) return;  // warp-uniform
-  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
+  const int64_t chunks = (N + ct - 1) / ct;
   const int64_t total = chunks * n;
   double G1 = 0.0, G2 = 0.0;
-  for (int i = lane; i < kChunkT; i += 32) {
+  for (int i = lane; i < ct; i += 32) {
     G1 += phipow[i];
     G2 += phipow[i] * phipow[i];
   }
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(kCarryThreads) synth_ar_carry_kernel(
     G1 += __shfl_xor_sync(0xffffffffu, G1, o);
     G2 += __shfl_xor_sync(0xffffffffu, G2, o);
   }
-  const double phiC = pow(phi, static_cast<double>(kChunkT));
+  const double phiC = pow(phi, static_cast<double>(ct));
   double x_in = state0[s];  // state before the current 32-chunk block
   double A = 0.0, B = 0.0;
   for (int64_t c0 = 0; c0 < chunks; c0 += 32) {
@@ -188,12 +194,12 @@ __global__ void __launch_bounds__(kCarryThreads) synth_ar_carry_kernel(
     int64_t len = 0;
     double a = 1.0, b = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, g1 = G1, g2 = G2;
     if (ok) {
-      len = min(static_cast<int64_t>(kChunkT), N - c * kChunkT);
+      len = min(static_cast<int64_t>(ct), N - c * ct);
       b = chunk_end[id];
       s1 = chunk_sums[id];
       s2 = chunk_sums[total + id];
       s3 = chunk_sums[2 * total + id];
-      if (len == kChunkT) {
+      if (len == ct) {
         a = phiC;
       } else {
         a = pow(phi, static_cast<double>(len));
@@ -291,16 +297,17 @@ __global__ void __launch_bounds__(256) col_moments_kernel(const double* X, int64
 // L(j,k) for j > k) and apply the Fleishman cubic (signals.cpp:241-248) in the
 // same pass.  Thread per time step, channels in groups of four loaded ahead
 // of the dependent running sum.
-__global__ void synth_std_mix_kernel(double* X, int n, int64_t N, const double* __restrict__ carry,
+__global__ void synth_std_mix_kernel(double* X, int n, int64_t N, int ct_log2, const double* __restrict__ carry,
                                      const double* __restrict__ phipow, const double* __restrict__ mean,
                                      const double* __restrict__ isd, const double* __restrict__ diag,
                                      const double* __restrict__ below, int mix, double fa, double fb, double fc,
                                      double fd) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= N) return;
-  const int64_t chunks = (N + kChunkT - 1) / kChunkT;
-  const double pw = phipow[t % kChunkT];
-  const double* cy = carry + t / kChunkT;
+  const int ct = 1 << ct_log2;
+  const int64_t chunks = (N + ct - 1) / ct;
+  const double pw = phipow[t & (ct - 1)];
+  const double* cy = carry + (t >> ct_log2);
   double acc = 0.0;
   double* x = X + t;
   int s = 0;

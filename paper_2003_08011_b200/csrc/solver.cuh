@@ -8,6 +8,7 @@
 // that already imported torch shares their pages.
 #pragma once
 
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 #include <dlfcn.h>
 
@@ -39,6 +40,44 @@ struct CusolverApi {
   cusolverStatus_t (*potrs)(cusolverDnHandle_t, cublasFillMode_t, int, int, const double*, int, double*, int,
                             int*) = nullptr;
 };
+
+// cuBLAS DGEMM (FP64 tensor-core path) for the train pipeline's one plain
+// library product, P = D_norm G+.  Bound lazily like cuSOLVER; null api.lib when absent.
+struct CublasApi {
+  void* lib = nullptr;
+  cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
+  cublasStatus_t (*destroy)(cublasHandle_t) = nullptr;
+  cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
+  cublasStatus_t (*dgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const double*,
+                          const double*, int, const double*, int, const double*, double*, int) = nullptr;
+};
+
+inline const CublasApi& cublas_api() {
+  static CublasApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* candidates[] = {
+        std::getenv("CSB_CUBLAS"),
+        "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib/libcublas.so.12",
+        "libcublas.so.12",
+        "/usr/local/cuda/lib64/libcublas.so.12",
+    };
+    for (const char* c : candidates) {
+      if (!c) continue;
+      if (void* h = dlopen(c, RTLD_NOW | RTLD_LOCAL)) {
+        api.lib = h;
+        break;
+      }
+    }
+    if (!api.lib) return;
+    api.create = reinterpret_cast<decltype(api.create)>(dlsym(api.lib, "cublasCreate_v2"));
+    api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.lib, "cublasDestroy_v2"));
+    api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(api.lib, "cublasSetStream_v2"));
+    api.dgemm = reinterpret_cast<decltype(api.dgemm)>(dlsym(api.lib, "cublasDgemm_v2"));
+    if (!api.create || !api.destroy || !api.set_stream || !api.dgemm) api.lib = nullptr;
+  });
+  return api;
+}
 
 inline const CusolverApi& cusolver_api() {
   static CusolverApi api;

@@ -18,6 +18,7 @@
 #include <vector>
 #include <chrono>
 #include <map>
+#include <functional>
 #include <mutex>
 #include <tuple>
 #include <type_traits>
@@ -272,6 +273,69 @@ bool cublas_handle(cs_ctx* ctx) {
   return bl.set_stream(ctx->blas, ctx->stream) == CUBLAS_STATUS_SUCCESS;
 }
 
+// G^-1 = L^-T L^-1 from the Cholesky factor L (lower, ld m) with DGEMMs on
+// the FP64 tensor-core path instead of potrs(L, I)'s two m-RHS TRSMs (2 m^3
+// flops at TRSM rates; 11.7 ms at m = 4000).  Both halves recurse on a 2 x 2
+// block split at multiples of 128:
+//   X = L^-1:  X11 = L11^-1, X22 = L22^-1, X21 = -X22 (L21 X11)
+//   C = X^T X: C11 = X11^T X11 + X21^T X21, C21 = X22^T X21, C22 = X22^T X22
+// ~2/3 m^3 flops each.  128-blocks: tri_inv_diag_kernel / one DGEMM.  Only
+// C's lower triangle is meaningful (the caller symmetrises).  Returns false
+// if cuBLAS is unavailable or a call fails (caller falls back to potrs).
+bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
+  if (!cublas_handle(ctx)) return false;
+  cudaStream_t st = ctx->stream;
+  const CublasApi& bl = cublas_api();
+  const int ld = static_cast<int>(m);
+  const size_t half = static_cast<size_t>((m + 1) / 2 + kTriInvB);
+  TmpBuf<double> X(static_cast<size_t>(m) * m), T(half * half);
+  CSB_CUDA(cudaMemsetAsync(X.get(), 0, m * m * sizeof(double), st));
+  CSB_CUDA(cudaMemsetAsync(out, 0, m * m * sizeof(double), st));
+  const size_t smem = sizeof(double) * kTriInvB * (kTriInvB + 1);
+  CSB_CUDA(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  tri_inv_diag_kernel<<<ceil_div(m, kTriInvB), kTriInvB, smem, st>>>(L, m, X.get());
+  CSB_LAUNCH_CHECK();
+  bool ok = true;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  auto gemm = [&](cublasOperation_t ta, int r, int c, int k, const double* alpha, const double* A, int lda,
+                  const double* B, int ldb, const double* beta, double* C, int ldc) {
+    if (ok && bl.dgemm(ctx->blas, ta, CUBLAS_OP_N, r, c, k, alpha, A, lda, B, ldb, beta, C, ldc) !=
+                  CUBLAS_STATUS_SUCCESS)
+      ok = false;
+  };
+  auto split = [](int64_t b) { return ((b / 2 + kTriInvB - 1) / kTriInvB) * kTriInvB; };
+  auto at = [&](const double* A, int64_t i, int64_t j) { return A + i + j * m; };
+  auto atw = [&](double* A, int64_t i, int64_t j) { return A + i + j * m; };
+  std::function<void(int64_t, int64_t)> inv = [&](int64_t r0, int64_t b) {
+    if (b <= kTriInvB) return;  // diagonal blocks done by the kernel
+    const int64_t b1 = split(b), b2 = b - b1, r1 = r0 + b1;
+    inv(r0, b1);
+    inv(r1, b2);
+    gemm(CUBLAS_OP_N, b2, b1, b1, &one, at(L, r1, r0), ld, at(X.get(), r0, r0), ld, &zero, T.get(),
+         static_cast<int>(b2));
+    gemm(CUBLAS_OP_N, b2, b1, b2, &mone, at(X.get(), r1, r1), ld, T.get(), static_cast<int>(b2), &zero,
+         atw(X.get(), r1, r0), ld);
+  };
+  std::function<void(int64_t, int64_t)> prod = [&](int64_t r0, int64_t b) {
+    if (b <= kTriInvB) {
+      gemm(CUBLAS_OP_T, b, b, b, &one, at(X.get(), r0, r0), ld, at(X.get(), r0, r0), ld, &zero,
+           atw(out, r0, r0), ld);
+      return;
+    }
+    const int64_t b1 = split(b), b2 = b - b1, r1 = r0 + b1;
+    prod(r0, b1);
+    gemm(CUBLAS_OP_T, b1, b1, b2, &one, at(X.get(), r1, r0), ld, at(X.get(), r1, r0), ld, &one,
+         atw(out, r0, r0), ld);
+    gemm(CUBLAS_OP_T, b2, b1, b2, &one, at(X.get(), r1, r1), ld, at(X.get(), r1, r0), ld, &zero,
+         atw(out, r1, r0), ld);
+    prod(r1, b2);
+  };
+  inv(0, m);
+  prod(0, m);
+  return ok;
+}
+
 // Full-rank fast path of the pseudo-inverse: when every eigenvalue passes the
 // reference cutoff (rank == m), G+ = V L^-1 V^T = G^-1 exactly, computed here
 // by Cholesky factorisation + inverse (~m^3 flops instead of syevd's vector
@@ -301,21 +365,31 @@ bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
     CSB_CUDA(cudaStreamSynchronize(st));
     if (h[0] != 0 || h[1] != 0) return false;
   } else {
-    // factor, then G^-1 = potrs(L, I): two triangular solves with m
-    // right-hand sides (cuBLAS TRSM, ~2 m^3 flops at GEMM-like rates); the
-    // in-place potri (trtri + lauum) was ~8x slower at m = 1000-4000
+    // factor, then G^-1 = L^-T L^-1 by the blocked DGEMM recursion
+    // (tri_inverse_product), or potrs(L, I) -- two triangular solves with m
+    // right-hand sides -- where cuBLAS is absent or CSB_POTRI=2; the in-place
+    // potri (trtri + lauum) was ~8x slower at m = 1000-4000, and cuSOLVER
+    // Xtrtri + DSYRK 40% slower than potrs at m = 2000-4000
     TmpBuf<double> L(static_cast<size_t>(m) * m);
     CSB_CUDA(cudaMemcpyAsync(L.get(), G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
     int l1 = 0;
     solver_check(api.potrf_buffer(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, L.get(), mi, &l1), "Dpotrf_bufferSize");
     TmpBuf<double> work(static_cast<size_t>(l1) + 1);
     TmpBuf<int> info(2);
+    CSB_CUDA(cudaMemsetAsync(info.get(), 0, 2 * sizeof(int), st));  // info[1] stays 0 on the blocked route
     solver_check(api.potrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, L.get(), mi, work.get(), l1, info.get()),
                  "Dpotrf");
-    set_identity_kernel<<<grid_for(m * m), 256, 0, st>>>(out, m);
-    CSB_LAUNCH_CHECK();
-    solver_check(api.potrs(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, mi, L.get(), mi, out, mi, info.get() + 1),
-                 "Dpotrs");
+    int hf = 0;
+    CSB_CUDA(cudaMemcpyAsync(&hf, info.get(), sizeof hf, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    if (hf != 0) return false;  // not numerically positive definite
+    const bool blocked = !(env && env[0] == '2') && tri_inverse_product(ctx, L.get(), m, out);
+    if (!blocked) {
+      set_identity_kernel<<<grid_for(m * m), 256, 0, st>>>(out, m);
+      CSB_LAUNCH_CHECK();
+      solver_check(api.potrs(ctx->solver, CUBLAS_FILL_MODE_LOWER, mi, mi, L.get(), mi, out, mi, info.get() + 1),
+                   "Dpotrs");
+    }
     int h[2] = {0, 0};
     CSB_CUDA(cudaMemcpyAsync(h, info.get(), sizeof h, cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaStreamSynchronize(st));

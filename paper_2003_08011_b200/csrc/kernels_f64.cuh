@@ -297,6 +297,34 @@ __global__ void set_identity_kernel(double* __restrict__ A, int64_t m) {
     A[e] = (e % m == e / m) ? 1.0 : 0.0;
 }
 
+// Inverse of each 128 x 128 diagonal block of a lower-triangular L (column-
+// major, ld m) into the same block of X (lower part; X pre-zeroed): one CTA
+// per block, thread j forward-substitutes column j of the block's inverse,
+// L's block staged in shared memory (pitch 129).  Base case of the blocked
+// triangular inversion in cstress_b200.cu (tri_inverse).
+constexpr int kTriInvB = 128;
+__global__ void __launch_bounds__(kTriInvB) tri_inv_diag_kernel(const double* __restrict__ L, int64_t m,
+                                                                double* __restrict__ X) {
+  extern __shared__ double Ls[];  // kTriInvB x (kTriInvB + 1)
+  constexpr int P = kTriInvB + 1;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kTriInvB;
+  const int b = static_cast<int>(min(static_cast<int64_t>(kTriInvB), m - r0));
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e % b, k = e / b;
+    Ls[i + k * P] = L[(r0 + i) + (r0 + k) * m];
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j >= b) return;
+  double* x = X + r0 + (r0 + j) * m;  // column j of the block
+  x[j] = 1.0 / Ls[j + j * P];
+  for (int i = j + 1; i < b; ++i) {
+    double acc = 0.0;
+    for (int k = j; k < i; ++k) acc = fma(Ls[i + k * P], x[k], acc);
+    x[i] = -acc / Ls[i + i * P];
+  }
+}
+
 // Mirror the lower triangle into the upper one (potri writes the lower
 // triangle of the inverse only; potrs's full result is made exactly
 // symmetric the same way).

@@ -32,9 +32,10 @@ def launches(path):
     h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[h]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    ni = hdr.index("Metric Name")
     agg = defaultdict(list)
     for r in rows[h + 1:]:
-        if len(r) > vi:
+        if len(r) > vi and r[ni] == "gpu__time_duration.sum":
             v = float(r[vi].replace(",", ""))
             if r[ui] == "usecond":
                 v *= 1e3

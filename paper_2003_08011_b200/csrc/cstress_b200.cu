@@ -318,11 +318,8 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
          atw(X.get(), r1, r0), ld);
   };
   std::function<void(int64_t, int64_t)> prod = [&](int64_t r0, int64_t b) {
-    if (b <= kTriInvB) {
-      gemm(CUBLAS_OP_T, b, b, b, &one, at(X.get(), r0, r0), ld, at(X.get(), r0, r0), ld, &zero,
-           atw(out, r0, r0), ld);
-      return;
-    }
+    if (b <= kTriInvB) return;  // diagonal blocks done up front (batched)
+
     const int64_t b1 = split(b), b2 = b - b1, r1 = r0 + b1;
     prod(r0, b1);
     gemm(CUBLAS_OP_T, b1, b1, b2, &one, at(X.get(), r1, r0), ld, at(X.get(), r1, r0), ld, &one,
@@ -332,6 +329,19 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
     prod(r1, b2);
   };
   inv(0, m);
+  // C's 128-aligned diagonal blocks X_bb^T X_bb first (one strided-batched
+  // DGEMM + the remainder block): the recursion only adds into them
+  const int64_t full = m / kTriInvB, rem = m - full * kTriInvB;
+  const long long stride = static_cast<long long>(kTriInvB) * (m + 1);
+  if (full > 0 && ok &&
+      bl.dgemm_strided(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, kTriInvB, kTriInvB, kTriInvB, &one, X.get(), ld, stride,
+                       X.get(), ld, stride, &zero, out, ld, stride, static_cast<int>(full)) != CUBLAS_STATUS_SUCCESS)
+    ok = false;
+  if (rem > 0) {
+    const int64_t r0 = full * kTriInvB;
+    gemm(CUBLAS_OP_T, rem, rem, rem, &one, at(X.get(), r0, r0), ld, at(X.get(), r0, r0), ld, &zero,
+         atw(out, r0, r0), ld);
+  }
   prod(0, m);
   return ok;
 }
@@ -515,7 +525,7 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
   M->p_shift.resize(n);
   M->scale_out_d.resize(n);
   M->scale_out_f.resize(n);
-  p_row_scale_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P.get(), M->scale.get(), n, m, M->p_shift.get(),
+  p_row_scale_kernel<<<ceil_div(n, 32), 1024, 0, st>>>(P.get(), M->scale.get(), n, m, M->p_shift.get(),
                                                          M->scale_out_d.get(), M->scale_out_f.get());
   CSB_LAUNCH_CHECK();
   if (M->tc) {

@@ -100,13 +100,23 @@ __global__ void pack_p_tiles_kernel(const double* __restrict__ P, const double* 
 // (1 for an all-zero row), and the estimate multipliers
 // scale_out = scale_s * 2^(k_s - 14) in FP64 and FP32 (exact power-of-two
 // rescaling of the FP64 scale).
-__global__ void p_row_scale_kernel(const double* __restrict__ P, const double* __restrict__ scale, int n, int m,
-                                   double* __restrict__ p_shift, double* __restrict__ scale_out_d,
-                                   float* __restrict__ scale_out_f) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
+// Block = 32 rows x 32 column slices (max is order-free: same result as a
+// sequential scan); row s's slice j scans columns j, j + 32, ...
+__global__ void __launch_bounds__(1024) p_row_scale_kernel(const double* __restrict__ P,
+                                                           const double* __restrict__ scale, int n, int m,
+                                                           double* __restrict__ p_shift,
+                                                           double* __restrict__ scale_out_d,
+                                                           float* __restrict__ scale_out_f) {
+  __shared__ double part[32][33];
+  const int r = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int s = blockIdx.x * 32 + r;
   double mx = 0.0;
-  for (int i = 0; i < m; ++i) mx = fmax(mx, fabs(P[s + static_cast<int64_t>(i) * n]));
+  if (s < n)
+    for (int i = j; i < m; i += 32) mx = fmax(mx, fabs(P[s + static_cast<int64_t>(i) * n]));
+  part[j][r] = mx;
+  __syncthreads();
+  if (j != 0 || s >= n) return;
+  for (int q = 1; q < 32; ++q) mx = fmax(mx, part[q][r]);
   int k = 0;
   if (mx > 0.0) {
     int ex;

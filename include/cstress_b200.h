@@ -197,6 +197,15 @@ cs_status cs_synthesize_uniform(int64_t n, int64_t N, double phi, double rho,
 cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double phi,
                                        double rho, double variance, double skewness,
                                        double kurtosis, uint64_t seed, double* d_out);
+/* Same feed, FP32 result: d_work (N x n FP64 scratch) holds the FP64 stream
+ * and the final variance-scale pass writes (float)(x * scale) into d_out32
+ * -- bit-identical to converting cs_synthesize_uniform_device's output,
+ * without the extra FP64 write and conversion pass (device-resident FP32
+ * surveillance blocks for the sweep).  Synchronous. */
+cs_status cs_synthesize_uniform_device_f32(cs_ctx* ctx, int64_t n, int64_t N, double phi,
+                                           double rho, double variance, double skewness,
+                                           double kurtosis, uint64_t seed, double* d_work,
+                                           float* d_out32);
 uint64_t cs_derive_seed(uint64_t parent, const uint64_t* coords, int ncoords);
 /* sweep.cpp:119-126 */
 uint64_t cs_cell_data_seed(uint64_t master_seed, int64_t n_signals,

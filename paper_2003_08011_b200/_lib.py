@@ -53,6 +53,7 @@ _SIGNATURES = {
     "cs_model_load": (i32, [vp, C.c_char_p, i32, P(vp)]),
     "cs_synthesize_uniform": (i32, [i64, i64, d, d, d, d, d, u64, pd]),
     "cs_synthesize_uniform_device": (i32, [vp, i64, i64, d, d, d, d, d, u64, vp]),
+    "cs_synthesize_uniform_device_f32": (i32, [vp, i64, i64, d, d, d, d, d, u64, vp, vp]),
     "cs_derive_seed": (u64, [u64, pu64, i32]),
     "cs_cell_data_seed": (u64, [u64, i64, i64, i64, i32]),
 }

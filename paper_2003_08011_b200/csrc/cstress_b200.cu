@@ -1426,9 +1426,33 @@ cs_status csb_prepare_uniform(int64_t n, int64_t N, double phi, double rho, doub
 bool csb_uniform_cholesky(int64_t n, double rho, std::vector<double>& diag, std::vector<double>& below);
 extern "C" {
 
+}  // extern "C"
+namespace {
+cs_status synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double phi, double rho, double variance,
+                                    double skewness, double kurtosis, uint64_t seed, double* d_out,
+                                    float* d_out32);
+}
+extern "C" {
+
 cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double phi, double rho,
                                        double variance, double skewness, double kurtosis,
                                        uint64_t seed, double* d_out) {
+  return synthesize_uniform_device(ctx, n, N, phi, rho, variance, skewness, kurtosis, seed, d_out, nullptr);
+}
+
+cs_status cs_synthesize_uniform_device_f32(cs_ctx* ctx, int64_t n, int64_t N, double phi, double rho,
+                                           double variance, double skewness, double kurtosis, uint64_t seed,
+                                           double* d_work, float* d_out32) {
+  if (!d_out32) return guarded([] { fail(CS_CONFIG_ERROR, "synthesize: null FP32 output"); });
+  return synthesize_uniform_device(ctx, n, N, phi, rho, variance, skewness, kurtosis, seed, d_work, d_out32);
+}
+
+}  // extern "C"
+
+namespace {
+cs_status synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double phi, double rho, double variance,
+                                    double skewness, double kurtosis, uint64_t seed, double* d_out,
+                                    float* d_out32) {
   double fc[4];
   const cs_status st0 = csb_prepare_uniform(n, N, phi, rho, variance, skewness, kurtosis, fc);
   if (st0 != CS_OK) return st0;
@@ -1476,11 +1500,17 @@ cs_status cs_synthesize_uniform_device(cs_ctx* ctx, int64_t n, int64_t N, double
     col_moments_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_out, N, mean.get(), sd.get());
     synth_scale_factor_kernel<<<ceil_div(n, 128), 128, 0, st>>>(sd.get(), static_cast<int>(n), variance,
                                                                 fscale.get());
-    synth_scale_kernel<<<dim3(nb, static_cast<unsigned>(n)), 256, 0, st>>>(d_out, N, fscale.get());
+    if (d_out32)
+      synth_scale_f32_kernel<<<dim3(nb, static_cast<unsigned>(n)), 256, 0, st>>>(d_out, N, fscale.get(), d_out32);
+    else
+      synth_scale_kernel<<<dim3(nb, static_cast<unsigned>(n)), 256, 0, st>>>(d_out, N, fscale.get());
     CSB_LAUNCH_CHECK();
     CSB_CUDA(cudaStreamSynchronize(st));
   });
 }
+}  // namespace
+
+extern "C" {
 
 cs_status cs_model_destroy(cs_model* M) {
   return guarded([&] {

@@ -350,4 +350,17 @@ __global__ void synth_scale_kernel(double* X, int64_t N, const double* __restric
   }
 }
 
+// FP32 result of the variance scale: out32 = (float)(X * f[s]) (the same
+// double product as synth_scale_kernel, then one rounding)
+__global__ void synth_scale_f32_kernel(const double* __restrict__ X, int64_t N, const double* __restrict__ f,
+                                       float* __restrict__ out32) {
+  const double g = f[blockIdx.y];
+  const int64_t off = static_cast<int64_t>(blockIdx.y) * N;
+#pragma unroll
+  for (int k = 0; k < kApplyT / 256; ++k) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kApplyT + k * 256 + threadIdx.x;
+    if (t < N) out32[off + t] = static_cast<float>(X[off + t] * g);
+  }
+}
+
 }  // namespace csb

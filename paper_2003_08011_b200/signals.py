@@ -54,18 +54,26 @@ def synthesize(spec: SignalSpec) -> SignalMatrix:
     return SignalMatrix(out, spec)
 
 
-def synthesize_device(spec: SignalSpec, device: int = 0):
-    """Same recipe on the GPU; returns an N x n column-major float64 torch
-    tensor on cuda:device (tolerance parity with ``synthesize``)."""
+def synthesize_device(spec: SignalSpec, device: int = 0, dtype=None):
+    """Same recipe on the GPU; returns an N x n column-major torch tensor on
+    cuda:device (tolerance parity with ``synthesize``).  float64 by default;
+    ``dtype=torch.float32`` rounds the final FP64 values once in the last
+    pass (bit-identical to ``synthesize_device(spec).float()``)."""
     import torch
     from .mset import context
-    out = torch.empty((spec.n_signals, spec.n_observations), dtype=torch.float64,
-                      device=torch.device("cuda", device)).T
+    dev = torch.device("cuda", device)
     ctx = context(device)
-    check(_lib.lib().cs_synthesize_uniform_device(
-        ctx.handle, spec.n_signals, spec.n_observations, spec.ar_coefficient,
-        spec.cross_correlation, spec.variance, spec.skewness, spec.kurtosis,
-        spec.seed & (2**64 - 1), out.data_ptr()))
+    args = (ctx.handle, spec.n_signals, spec.n_observations, spec.ar_coefficient, spec.cross_correlation,
+            spec.variance, spec.skewness, spec.kurtosis, spec.seed & (2**64 - 1))
+    if dtype is None or dtype == torch.float64:
+        out = torch.empty((spec.n_signals, spec.n_observations), dtype=torch.float64, device=dev).T
+        check(_lib.lib().cs_synthesize_uniform_device(*args, out.data_ptr()))
+        return out
+    if dtype != torch.float32:
+        raise ValueError("synthesize_device: dtype must be float64 or float32")
+    work = torch.empty((spec.n_signals, spec.n_observations), dtype=torch.float64, device=dev)
+    out = torch.empty((spec.n_signals, spec.n_observations), dtype=torch.float32, device=dev).T
+    check(_lib.lib().cs_synthesize_uniform_device_f32(*args, work.data_ptr(), out.data_ptr()))
     return out
 
 

@@ -28,6 +28,25 @@ def test_device_synthesis_matches_host(p, args):
     assert np.abs(dev - host).max() <= 1e-9 * np.abs(host).max()
 
 
+def test_device_synthesis_long_chunks(p):
+    # n x N large enough for the longest chunk length (1024) and a ragged
+    # last chunk; the shapes above run 32-128 sample chunks
+    args = (80, 1_000_000, 0.5, 0.3, 1.0, 0.5, 4.0, 20260810)
+    host = p.synthesize(p.SignalSpec.uniform(*args)).data
+    dev = p.synthesize_device(p.SignalSpec.uniform(*args)).cpu().numpy()
+    assert np.abs(dev - host).max() <= 1e-9 * np.abs(host).max()
+
+
+def test_device_synthesis_fp32_output(p):
+    import torch
+    for args in [(7, 3000, 0.5, 0.3, 1.0, 0.5, 4.0, 5), (100, 100_000, 0.5, 0.3, 1.0, 0.5, 4.0, 6)]:
+        spec = p.SignalSpec.uniform(*args)
+        a = p.synthesize_device(spec).float()
+        b = p.synthesize_device(spec, dtype=torch.float32)
+        assert b.dtype == torch.float32 and b.shape == a.shape and b.stride() == a.stride()
+        assert torch.equal(a, b)
+
+
 def test_device_synthesis_statistics(p):
     x = p.synthesize_device(p.SignalSpec.uniform(2, 200000, 0.8, 0.9, 1.0, 0.0, 3.0, 11)).cpu().numpy()
     assert 0.85 < np.corrcoef(x[:, 0], x[:, 1])[0, 1] < 0.95

@@ -287,8 +287,7 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
   cudaStream_t st = ctx->stream;
   const CublasApi& bl = cublas_api();
   const int ld = static_cast<int>(m);
-  const size_t half = static_cast<size_t>((m + 1) / 2 + kTriInvB);
-  TmpBuf<double> X(static_cast<size_t>(m) * m), T(half * half);
+  TmpBuf<double> X(static_cast<size_t>(m) * m);
   CSB_CUDA(cudaMemsetAsync(X.get(), 0, m * m * sizeof(double), st));
   CSB_CUDA(cudaMemsetAsync(out, 0, m * m * sizeof(double), st));
   const size_t smem = sizeof(double) * kTriInvB * (kTriInvB + 1);
@@ -304,33 +303,82 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
                   CUBLAS_STATUS_SUCCESS)
       ok = false;
   };
-  auto split = [](int64_t b) { return ((b / 2 + kTriInvB - 1) / kTriInvB) * kTriInvB; };
+  // Split tree: node (r0, b) -> (r0, b1), (r0 + b1, b2), b1 = b/2 rounded up
+  // to a multiple of 128.  Nodes of one depth are independent; both passes
+  // run deepest level first (children complete before their parent reads X11
+  // / X22, or adds into C11 over the children's beta = 0 writes), and each
+  // level's nodes of equal (b1, b2) go to cuBLAS as one batched DGEMM.
+  struct Node {
+    int64_t r0, b1, b2;
+  };
+  std::vector<std::vector<Node>> levels;
+  std::function<void(int64_t, int64_t, size_t)> build = [&](int64_t r0, int64_t b, size_t d) {
+    if (b <= kTriInvB) return;
+    const int64_t b1 = ((b / 2 + kTriInvB - 1) / kTriInvB) * kTriInvB, b2 = b - b1;
+    if (levels.size() <= d) levels.resize(d + 1);
+    levels[d].push_back({r0, b1, b2});
+    build(r0, b1, d + 1);
+    build(r0 + b1, b2, d + 1);
+  };
+  build(0, m, 0);
+  size_t tmp_el = 0, max_batch = 1;
+  for (const auto& lv : levels) {
+    size_t el = 0;
+    for (const Node& q : lv) el += static_cast<size_t>(q.b1 * q.b2);
+    tmp_el = std::max(tmp_el, el);
+    max_batch = std::max(max_batch, lv.size());
+  }
+  TmpBuf<double> T(tmp_el + 1);
+  TmpBuf<const double*> ptrs(6 * max_batch);
   auto at = [&](const double* A, int64_t i, int64_t j) { return A + i + j * m; };
-  auto atw = [&](double* A, int64_t i, int64_t j) { return A + i + j * m; };
-  std::function<void(int64_t, int64_t)> inv = [&](int64_t r0, int64_t b) {
-    if (b <= kTriInvB) return;  // diagonal blocks done by the kernel
-    const int64_t b1 = split(b), b2 = b - b1, r1 = r0 + b1;
-    inv(r0, b1);
-    inv(r1, b2);
-    gemm(CUBLAS_OP_N, b2, b1, b1, &one, at(L, r1, r0), ld, at(X.get(), r0, r0), ld, &zero, T.get(),
-         static_cast<int>(b2));
-    gemm(CUBLAS_OP_N, b2, b1, b2, &mone, at(X.get(), r1, r1), ld, T.get(), static_cast<int>(b2), &zero,
-         atw(X.get(), r1, r0), ld);
+  // one batched DGEMM per (b1, b2) group of a level: C_i = alpha op(A_i) B_i + beta C_i
+  auto batched = [&](cublasOperation_t ta, int r, int c, int k, const double* alpha,
+                     const std::vector<const double*>& A, int lda, const std::vector<const double*>& B, int ldb,
+                     const double* beta, const std::vector<const double*>& C, int ldc) {
+    if (!ok) return;
+    if (A.size() == 1) {
+      gemm(ta, r, c, k, alpha, A[0], lda, B[0], ldb, beta, const_cast<double*>(C[0]), ldc);
+      return;
+    }
+    const size_t nb = A.size();
+    std::vector<const double*> h(3 * nb);
+    std::copy(A.begin(), A.end(), h.begin());
+    std::copy(B.begin(), B.end(), h.begin() + nb);
+    std::copy(C.begin(), C.end(), h.begin() + 2 * nb);
+    CSB_CUDA(cudaMemcpyAsync(ptrs.get(), h.data(), 3 * nb * sizeof(double*), cudaMemcpyHostToDevice, st));
+    // the pointer table is reused by the next call: keep the copy ordered
+    // before it (pageable H2D returns once staged; the stream orders the rest)
+    if (bl.dgemm_batched(ctx->blas, ta, CUBLAS_OP_N, r, c, k, alpha, ptrs.get(), lda, ptrs.get() + nb, ldb, beta,
+                         const_cast<double* const*>(ptrs.get() + 2 * nb), ldc,
+                         static_cast<int>(nb)) != CUBLAS_STATUS_SUCCESS)
+      ok = false;
   };
-  std::function<void(int64_t, int64_t)> prod = [&](int64_t r0, int64_t b) {
-    if (b <= kTriInvB) return;  // diagonal blocks done up front (batched)
-
-    const int64_t b1 = split(b), b2 = b - b1, r1 = r0 + b1;
-    prod(r0, b1);
-    gemm(CUBLAS_OP_T, b1, b1, b2, &one, at(X.get(), r1, r0), ld, at(X.get(), r1, r0), ld, &one,
-         atw(out, r0, r0), ld);
-    gemm(CUBLAS_OP_T, b2, b1, b2, &one, at(X.get(), r1, r1), ld, at(X.get(), r1, r0), ld, &zero,
-         atw(out, r1, r0), ld);
-    prod(r1, b2);
+  auto groups = [](const std::vector<Node>& lv) {
+    std::map<std::pair<int64_t, int64_t>, std::vector<Node>> g;
+    for (const Node& q : lv) g[{q.b1, q.b2}].push_back(q);
+    return g;
   };
-  inv(0, m);
+  // X = L^-1: T_i = L21 X11, X21 = -X22 T_i
+  for (size_t d = levels.size(); d-- > 0;) {
+    size_t toff = 0;
+    for (const auto& kv : groups(levels[d])) {
+      const int64_t b1 = kv.first.first, b2 = kv.first.second;
+      std::vector<const double*> A1, B1, C1, A2, C2;
+      for (const Node& q : kv.second) {
+        const int64_t r1 = q.r0 + b1;
+        A1.push_back(at(L, r1, q.r0));
+        B1.push_back(at(X.get(), q.r0, q.r0));
+        C1.push_back(T.get() + toff);
+        A2.push_back(at(X.get(), r1, r1));
+        C2.push_back(at(X.get(), r1, q.r0));
+        toff += static_cast<size_t>(b1 * b2);
+      }
+      batched(CUBLAS_OP_N, b2, b1, b1, &one, A1, ld, B1, ld, &zero, C1, static_cast<int>(b2));
+      batched(CUBLAS_OP_N, b2, b1, b2, &mone, A2, ld, C1, static_cast<int>(b2), &zero, C2, ld);
+    }
+  }
   // C's 128-aligned diagonal blocks X_bb^T X_bb first (one strided-batched
-  // DGEMM + the remainder block): the recursion only adds into them
+  // DGEMM + the remainder block): the levels only add into them
   const int64_t full = m / kTriInvB, rem = m - full * kTriInvB;
   const long long stride = static_cast<long long>(kTriInvB) * (m + 1);
   if (full > 0 && ok &&
@@ -340,9 +388,24 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
   if (rem > 0) {
     const int64_t r0 = full * kTriInvB;
     gemm(CUBLAS_OP_T, rem, rem, rem, &one, at(X.get(), r0, r0), ld, at(X.get(), r0, r0), ld, &zero,
-         atw(out, r0, r0), ld);
+         out + r0 + r0 * m, ld);
   }
-  prod(0, m);
+  // C = X^T X: C11 += X21^T X21, C21 = X22^T X21
+  for (size_t d = levels.size(); d-- > 0;) {
+    for (const auto& kv : groups(levels[d])) {
+      const int64_t b1 = kv.first.first, b2 = kv.first.second;
+      std::vector<const double*> X21, X22, C11, C21;
+      for (const Node& q : kv.second) {
+        const int64_t r1 = q.r0 + b1;
+        X21.push_back(at(X.get(), r1, q.r0));
+        X22.push_back(at(X.get(), r1, r1));
+        C11.push_back(at(out, q.r0, q.r0));
+        C21.push_back(at(out, r1, q.r0));
+      }
+      batched(CUBLAS_OP_T, b1, b1, b2, &one, X21, ld, X21, ld, &one, C11, ld);
+      batched(CUBLAS_OP_T, b2, b1, b2, &one, X22, ld, X21, ld, &zero, C21, ld);
+    }
+  }
   return ok;
 }
 

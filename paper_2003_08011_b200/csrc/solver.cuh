@@ -50,6 +50,9 @@ struct CublasApi {
   cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
   cublasStatus_t (*dgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const double*,
                           const double*, int, const double*, int, const double*, double*, int) = nullptr;
+  cublasStatus_t (*dgemm_batched)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                                  const double*, const double* const*, int, const double* const*, int,
+                                  const double*, double* const*, int, int) = nullptr;
   cublasStatus_t (*dgemm_strided)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
                                   const double*, const double*, int, long long, const double*, int, long long,
                                   const double*, double*, int, long long, int) = nullptr;
@@ -77,9 +80,10 @@ inline const CublasApi& cublas_api() {
     api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(api.lib, "cublasDestroy_v2"));
     api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(api.lib, "cublasSetStream_v2"));
     api.dgemm = reinterpret_cast<decltype(api.dgemm)>(dlsym(api.lib, "cublasDgemm_v2"));
+    api.dgemm_batched = reinterpret_cast<decltype(api.dgemm_batched)>(dlsym(api.lib, "cublasDgemmBatched"));
     api.dgemm_strided =
         reinterpret_cast<decltype(api.dgemm_strided)>(dlsym(api.lib, "cublasDgemmStridedBatched"));
-    if (!api.create || !api.destroy || !api.set_stream || !api.dgemm || !api.dgemm_strided) api.lib = nullptr;
+    if (!api.create || !api.destroy || !api.set_stream || !api.dgemm || !api.dgemm_strided || !api.dgemm_batched) api.lib = nullptr;
   });
   return api;
 }

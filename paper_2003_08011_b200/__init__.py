@@ -15,3 +15,4 @@ from .estimator import (MeanPredictor, MsetAlgorithm, PrognosticAlgorithm,  # no
 from .signals import (SignalMatrix, SignalSpec, cell_data_seed, derive_seed, synthesize,  # noqa: F401
                       synthesize_device)
 from .sprt import SprtDetector, residual_sigma, sprt_params  # noqa: F401,E402
+from . import surfaces  # noqa: F401,E402

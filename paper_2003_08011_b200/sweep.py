@@ -138,14 +138,22 @@ class CostCell:
         if not s:
             self.mean = self.median = self.stddev = 0.0
             return
-        self.mean = sum(s) / len(s)
+        # plain left-to-right loops as in the reference (Python >= 3.12's
+        # sum() of floats is compensated and can differ in the last bit)
+        mean = 0.0
+        for x in s:
+            mean += x
+        self.mean = mean / float(len(s))
         srt = sorted(s)
         h = len(srt) // 2
         self.median = srt[h] if len(srt) % 2 == 1 else 0.5 * (srt[h - 1] + srt[h])
         if len(s) < 2:
             self.stddev = 0.0
         else:
-            self.stddev = math.sqrt(sum((x - self.mean) ** 2 for x in s) / (len(s) - 1))
+            ss = 0.0
+            for x in s:
+                ss += (x - self.mean) * (x - self.mean)
+            self.stddev = math.sqrt(ss / (float(len(s)) - 1.0))
 
 
 @dataclass

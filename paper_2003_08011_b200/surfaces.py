@@ -180,3 +180,103 @@ def export_speedup_csv(surface: SpeedupSurface, phase: Phase, path: str) -> None
                 f.write(row + "\n")
     except OSError as e:
         raise IoError(f"export_speedup_csv: cannot open {path}") from e
+
+
+# ------------------------------------------------------------ surface JSON
+SURFACE_FORMAT = "containerstress-surface"  # surfaces.cpp:442-443
+
+
+def backend_to_json(b: BackendId):
+    """config.cpp:172-177, extended with the b200 kind."""
+    return {"kind": b.kind, "device": b.device, "precision": b.precision}
+
+
+def backend_from_json(j) -> BackendId:
+    if not isinstance(j, dict) or j.get("kind") != "b200":
+        raise ConfigError(f"unknown backend id: {j!r}")
+    b = BackendId("b200", int(j["device"]), str(j["precision"]))
+    b.validate()
+    return b
+
+
+def _metadata_json(surface: CostSurface) -> dict:
+    m = dict(surface.metadata)
+    caps = m.get("backend_capabilities", [])
+    if caps and not isinstance(caps[0], dict):  # run_sweep form: descriptions in backend order
+        caps = [{"backend": backend_to_json(b), "deterministic_summation": True, "description": d}
+                for b, d in zip(surface_backends(surface), caps)]
+    known = {"generator", "host_description", "host", "hardware_threads", "timer", "rng_algorithm", "started_at",
+             "finished_at", "threads_override", "partial", "config", "backend_capabilities"}
+    config = dict(m.get("config", {}))
+    config.update({k: v for k, v in m.items() if k not in known})  # world_size, placement, ...
+    return {"generator": m.get("generator", ""), "host": m.get("host", m.get("host_description", "")),
+            "hardware_threads": int(m.get("hardware_threads") or 0), "timer": m.get("timer", ""),
+            "rng_algorithm": m.get("rng_algorithm", ""), "started_at": m.get("started_at", ""),
+            "finished_at": m.get("finished_at", ""), "threads_override": m.get("threads_override", ""),
+            "partial": bool(m.get("partial", False)), "config": config, "backend_capabilities": caps}
+
+
+def surface_to_json(surface: CostSurface) -> dict:
+    """surfaces.cpp:418-459."""
+    cells = []
+    for c in surface.cells:
+        jc = {"phase": c.phase.value, "backend": backend_to_json(c.backend), "n_signals": c.coords.n_signals,
+              "n_observations": c.coords.n_observations, "n_memory": c.coords.n_memory,
+              "excluded": c.excluded, "reason": c.reason, "samples": list(c.samples),
+              "data_seeds": list(c.data_seeds)}
+        if c.samples:
+            jc["median_s"], jc["mean_s"], jc["std_s"] = c.median, c.mean, c.stddev
+        cells.append(jc)
+    return {"format": SURFACE_FORMAT, "version": 1, "metadata": _metadata_json(surface), "cells": cells}
+
+
+def surface_from_json(j: dict) -> CostSurface:
+    """surfaces.cpp:461-507 (aggregates recomputed from the samples)."""
+    try:
+        if j["format"] != SURFACE_FORMAT:
+            raise IoError("surface: unexpected format tag")
+        if j["version"] != 1:
+            raise IoError("surface: unsupported version")
+        meta = dict(j["metadata"])
+        meta["backend_capabilities"] = [
+            {"backend": backend_to_json(backend_from_json(c["backend"])),
+             "deterministic_summation": bool(c["deterministic_summation"]), "description": str(c["description"])}
+            for c in meta["backend_capabilities"]]
+        cells = []
+        for jc in j["cells"]:
+            if jc["phase"] not in ("train", "surveil"):
+                raise ConfigError("unknown phase: " + str(jc["phase"]))
+            c = CostCell(CellCoords(int(jc["n_signals"]), int(jc["n_observations"]), int(jc["n_memory"])),
+                         Phase(jc["phase"]), backend_from_json(jc["backend"]))
+            c.excluded = bool(jc["excluded"])
+            c.reason = str(jc["reason"])
+            c.samples = [float(x) for x in jc["samples"]]
+            c.data_seeds = [int(x) for x in jc["data_seeds"]]
+            c.recompute_aggregates()
+            cells.append(c)
+        return CostSurface(cells, meta)
+    except (KeyError, TypeError, ValueError) as e:
+        raise IoError(f"surface: malformed JSON: {e}") from None
+
+
+def export_surface_json(surface: CostSurface, path: str) -> None:
+    """surfaces.cpp:509-514: nlohmann dump(2) layout (sorted keys, two-space
+    indent, shortest round-trip doubles) plus a trailing newline."""
+    import json
+    try:
+        with open(path, "w", encoding="utf-8", newline="") as f:
+            f.write(json.dumps(surface_to_json(surface), indent=2, sort_keys=True, ensure_ascii=False) + "\n")
+    except OSError as e:
+        raise IoError(f"export_surface_json: cannot open {path}") from e
+
+
+def import_surface_json(path: str) -> CostSurface:
+    import json
+    try:
+        with open(path, encoding="utf-8") as f:
+            j = json.load(f)
+    except OSError:
+        raise IoError(f"import_surface_json: cannot open {path}") from None
+    except ValueError as e:
+        raise IoError(f"surface: malformed JSON: {e}") from None
+    return surface_from_json(j)

@@ -99,3 +99,31 @@ def test_sweep_large_cell_runs(p):
     cfg.signal_template.skewness, cfg.signal_template.kurtosis = 0.5, 4.0
     cells = run_cell(CellCoords(100, 100_000, 1000), cfg)
     assert not any(c.excluded for c in cells)
+
+
+def test_sweep_surface_files_and_speedup(p, tmp_path):
+    # acceptance.cpp:368-414 analogue: a two-backend sweep's cost CSV and
+    # surface JSON re-export byte-identically; the speedup surface of the
+    # FP64 path over the tcgen05 FP32 path has the grid's holes
+    from paper_2003_08011_b200 import BackendId
+    from paper_2003_08011_b200.surfaces import (cells_for_phase, export_cost_csv, export_speedup_csv,
+                                                export_surface_json, import_cost_csv, import_surface_json,
+                                                speedup)
+    from paper_2003_08011_b200.sweep import Phase, SweepConfig, SweepGrid, run_sweep
+    f64, f32 = BackendId("b200", 0, "fp64"), BackendId("b200", 0, "fp32")
+    cfg = SweepConfig(SweepGrid([2, 8], [2000], [8, 64]), replicates=2, warmups=1, master_seed=20260810,
+                      backends=[f64, f32])
+    s = run_sweep(cfg)
+    c1, c2 = tmp_path / "c1.csv", tmp_path / "c2.csv"
+    export_cost_csv(cells_for_phase(s, Phase.train), str(c1))
+    export_cost_csv(import_cost_csv(str(c1)), str(c2))
+    assert c1.read_bytes() == c2.read_bytes()
+    j1, j2 = tmp_path / "s1.json", tmp_path / "s2.json"
+    export_surface_json(s, str(j1))
+    export_surface_json(import_surface_json(str(j1)), str(j2))
+    assert j1.read_bytes() == j2.read_bytes()
+    sp = speedup(s, f64, f32)
+    holes = [c for c in sp.cells if c.hole]
+    assert len(holes) == 2 and all(c.reason == "m<2n" for c in holes)  # (8, 2000, 8) train + surveil
+    assert all(c.speedup > 0 for c in sp.cells if not c.hole)
+    export_speedup_csv(sp, Phase.surveil, str(tmp_path / "sp.csv"))

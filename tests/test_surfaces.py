@@ -116,3 +116,31 @@ def test_speedup_csv_export(tmp_path):
                            "n_memory,hole,reason,speedup\n")
     assert f"train,{REF.label()},{OPT.label()},2,64,8,false,,2\n" in text
     assert "surveil," not in text
+
+
+def test_surface_json_round_trip_byte_identical(tmp_path):
+    from paper_2003_08011_b200.surfaces import export_surface_json, import_surface_json
+    cells = [make_cell(2, 64, 8, Phase.train, REF, 0.125), make_cell(2, 64, 8, Phase.surveil, OPT, 1e-05),
+             make_excluded(8, 64, 8, Phase.train, REF, "m<2n")]
+    cells[0].samples = [0.1, 0.2, 0.30000001]
+    cells[0].data_seeds = [2**64 - 1, 12345, 0]
+    cells[0].recompute_aggregates()
+    meta = {"generator": "containerstress-b200 0.1.0", "host_description": "x86_64 / Linux",
+            "hardware_threads": 16, "timer": "wall_monotonic", "rng_algorithm": "splitmix64",
+            "world_size": 2, "placement": "LPT", "started_at": "2026-10-17T00:00:00Z",
+            "finished_at": "2026-10-17T00:00:01Z", "backend_capabilities": ["fp64 path", "fp32 path"]}
+    s1, s2 = tmp_path / "s1.json", tmp_path / "s2.json"
+    export_surface_json(CostSurface(cells, meta), str(s1))
+    back = import_surface_json(str(s1))
+    assert [c.samples for c in back.cells] == [c.samples for c in cells]
+    assert back.cells[0].data_seeds == cells[0].data_seeds
+    assert back.cells[0].median == cells[0].median and back.cells[2].excluded
+    assert back.cells[1].backend == OPT
+    export_surface_json(back, str(s2))
+    assert s1.read_bytes() == s2.read_bytes()
+    text = s1.read_text()
+    assert '"format": "containerstress-surface"' in text and '"version": 1' in text
+    bad = tmp_path / "bad.json"
+    bad.write_text(text.replace("containerstress-surface", "other"))
+    with pytest.raises(IoError):
+        import_surface_json(str(bad))

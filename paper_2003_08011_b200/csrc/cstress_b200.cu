@@ -409,6 +409,35 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
   return ok;
 }
 
+// Gram matrix of a model's normalised memory vectors (mset.cpp:151-152).
+// FP64-precision models: `sim_exact`, the reference's loop order bit for bit.
+// FP32-precision models (tolerance contract) at m >= 512: S = D_norm^T D_norm
+// as a cuBLAS DGEMM on the FP64 tensor-core path, then the kernel map of
+// ||d_i||^2 + ||d_j||^2 - 2 S_ij (2 n m^2 flops at DGEMM rate instead of
+// 3 n m^2 on CUDA cores; C3: 3.2 -> 1.2 ms).  Deterministic, so the lazy
+// eigen_spectrum re-forms the identical matrix.  CSB_GRAM_EXACT=1 forces the
+// exact kernel for every model.
+void form_gram(cs_ctx* ctx, const cs_model* M, double* gram) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = M->n, m = M->m;
+  const char* env = std::getenv("CSB_GRAM_EXACT");
+  const bool exact = (env && env[0] == '1') || M->precision != CS_PRECISION_FP32 || m < 512;
+  if (!exact && cublas_handle(ctx)) {
+    TmpBuf<double> dd(m);
+    col_sqnorm_kernel<<<ceil_div(m, 128), 128, 0, st>>>(M->Dn.get(), n, m, dd.get());
+    CSB_LAUNCH_CHECK();
+    const double one = 1.0, zero = 0.0;
+    if (cublas_api().dgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(m), static_cast<int>(m),
+                           static_cast<int>(n), &one, M->Dn.get(), static_cast<int>(n), M->Dn.get(),
+                           static_cast<int>(n), &zero, gram, static_cast<int>(m)) == CUBLAS_STATUS_SUCCESS) {
+      gram_from_dot_kernel<<<grid_for(m * m), 256, 0, st>>>(gram, dd.get(), m, M->kind, M->h);
+      CSB_LAUNCH_CHECK();
+      return;
+    }
+  }
+  launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, M->kind, M->h, gram, m);
+}
+
 // Full-rank fast path of the pseudo-inverse: when every eigenvalue passes the
 // reference cutoff (rank == m), G+ = V L^-1 V^T = G^-1 exactly, computed here
 // by Cholesky factorisation + inverse (~m^3 flops instead of syevd's vector
@@ -666,8 +695,8 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   CSB_LAUNCH_CHECK();
   TmpBuf<double> gram(m * m);                                // mset.cpp:151-152
   trace.mark("scale + normalise");
-  launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, kind, M->h, gram.get(), m);
-  trace.mark("gram (sim_exact)");
+  form_gram(ctx, M.get(), gram.get());
+  trace.mark("gram");
   // Pseudo-inverse (mset.cpp:153-170).  Fast path: Cholesky inverse of G,
   // certified full rank -- every eigenvalue of the SPD matrix G satisfies
   // lambda_min / lambda_max >= 1 / (||G||_1 ||G^-1||_1), so a 1-norm
@@ -1119,9 +1148,9 @@ void materialize_spectrum(const cs_model* M) {
   if (cs_ctx_create(M->device, &ctx) != CS_OK) fail(CS_ERROR, "eigen_spectrum: " + g_last_error);
   std::unique_ptr<cs_ctx, cs_status (*)(cs_ctx*)> guard(ctx, cs_ctx_destroy);
   StreamScope scope(ctx->stream);
-  const int64_t n = M->n, m = M->m;
+  const int64_t m = M->m;
   TmpBuf<double> gram(m * m), V(m * m);
-  launch_sim_exact(ctx->stream, M->Dn.get(), n, M->Dn.get(), n, n, m, m, M->kind, M->h, gram.get(), m);
+  form_gram(ctx, M, gram.get());
   M->spectrum.resize(m);
   eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), false);
   CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),

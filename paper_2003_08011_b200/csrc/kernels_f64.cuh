@@ -346,6 +346,30 @@ __global__ void __launch_bounds__(kTriInvB) tri_inv_diag_kernel(const double* __
   }
 }
 
+// ||D(:, i)||^2 for the GEMM-form Gram matrix (FP32-precision models)
+__global__ void col_sqnorm_kernel(const double* __restrict__ D, int64_t n, int64_t m, double* __restrict__ dd) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  double a = 0.0;
+  for (int64_t r = 0; r < n; ++r) a = fma(D[r + i * n], D[r + i * n], a);
+  dd[i] = a;
+}
+// G(i, j) = k(max(dd_i + dd_j - 2 S(i, j), 0)) from S = D^T D (lower triangle
+// read, both triangles written: G exactly symmetric), unit diagonal exact
+__global__ void gram_from_dot_kernel(double* __restrict__ G, const double* __restrict__ dd, int64_t m, int kind,
+                                     double h) {
+  const int64_t total = m * m;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    if (i < j) continue;
+    const double v = i == j ? kernel_from_d2(0.0, kind, h)
+                            : kernel_from_d2(fmax(dd[i] + dd[j] - 2.0 * G[e], 0.0), kind, h);
+    G[e] = v;
+    G[j + i * m] = v;
+  }
+}
+
 // Mirror the lower triangle into the upper one (potri writes the lower
 // triangle of the inverse only; potrs's full result is made exactly
 // symmetric the same way).

@@ -23,6 +23,14 @@ class MsetModel(PrognosticModel):
         self.model = model
 
 
+class HostMsetModel(PrognosticModel):
+    """A model trained by a registered host (CPU) backend."""
+
+    def __init__(self, model, kind: str):
+        self.model = model
+        self.kind = kind
+
+
 class MeanModel(PrognosticModel):
     def __init__(self, means):
         self.means = means
@@ -48,14 +56,54 @@ class PrognosticAlgorithm:
         raise NotImplementedError
 
 
+# Host (CPU) implementations of the reference's own backend kinds
+# ("reference", "optimized"; backends.hpp:14-33).  The B200 library never
+# computes on the CPU; a host implementation is registered by whoever wants
+# CPU cells in the same CostSurface as the b200 cells (the reference runs
+# every backend of a replicate inside one run_cell, sweep.cpp:206-227) --
+# here the benchmark's baseline leg and the tests, which register the CPU
+# oracle.  An implementation provides
+#   train(X, m, kernel: KernelConfig, backend) -> opaque host model
+#   estimate(model, observations, backend) -> (estimates, residuals)
+_HOST_BACKENDS: dict = {}
+
+
+def register_host_backend(kind: str, impl) -> None:
+    if kind not in mset.HOST_KINDS:
+        raise ConfigError("unknown host backend kind: " + kind)
+    _HOST_BACKENDS[kind] = impl
+
+
+def unregister_host_backend(kind: str) -> None:
+    _HOST_BACKENDS.pop(kind, None)
+
+
+def host_backend(backend: BackendId):
+    backend.validate()
+    impl = _HOST_BACKENDS.get(backend.kind)
+    if impl is None:
+        raise ConfigError(f"backend {backend.label()} has no host implementation registered "
+                          "(this library computes only on the B200)")
+    return impl
+
+
 class MsetAlgorithm(PrognosticAlgorithm):
     def name(self):
         return "mset2"
 
     def train(self, training, n_memory, kernel=KernelConfig(), backend=BackendId()):
+        if backend.is_host:
+            X = np.asfortranarray(np.asarray(getattr(training, "data", training), dtype=np.float64))
+            return HostMsetModel(host_backend(backend).train(X, n_memory, kernel, backend), backend.kind)
         return MsetModel(mset.train(training, n_memory, kernel, backend))
 
     def estimate(self, model, observations, backend=BackendId()):
+        if backend.is_host:
+            impl = host_backend(backend)
+            hm = _as(model, HostMsetModel, "mset2")
+            obs = np.asfortranarray(np.asarray(getattr(observations, "data", observations), dtype=np.float64))
+            est, res = impl.estimate(hm.model, obs, backend)
+            return EstimationResult(est, res)
         return mset.estimate(_as(model, MsetModel, "mset2").model, observations, backend)
 
 

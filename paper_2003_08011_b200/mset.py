@@ -67,8 +67,20 @@ class BackendId:
     kind: str = "b200"
     device: int = 0
     precision: str = "fp64"
+    # the reference's host kinds ("reference" / "optimized", backends.hpp:14-33)
+    # exist so that CPU and GPU cells share one CostSurface; this library does
+    # not compute them -- see register_host_backend
+    worker_count: int = 1
+    tile_size: int = 64
 
     def validate(self) -> None:
+        if self.kind in HOST_KINDS:  # backends.cpp:86-92
+            if self.kind == "optimized":
+                if self.worker_count < 1:
+                    raise ConfigError("backend worker_count must be >= 1")
+                if self.tile_size < 8 or self.tile_size > 1024:
+                    raise ConfigError("backend tile_size must lie in [8, 1024]")
+            return
         if self.kind != "b200":
             raise ConfigError(f"unknown backend id: {self.kind}")
         if self.device < 0:
@@ -76,17 +88,46 @@ class BackendId:
         if self.precision not in PRECISIONS:
             raise ConfigError(f"unknown precision: {self.precision}")
 
+    @property
+    def is_host(self) -> bool:
+        return self.kind in HOST_KINDS
+
     def label(self) -> str:
+        if self.kind == "reference":  # backends.cpp:94-99
+            return "reference"
+        if self.kind == "optimized":
+            return f"optimized[tile={self.tile_size}/workers={self.worker_count}]"
         return f"b200[device={self.device}/precision={self.precision}]"
+
+    @staticmethod
+    def reference() -> "BackendId":
+        return BackendId("reference")
+
+    @staticmethod
+    def optimized(workers: int = 0, tile: int = 64) -> "BackendId":
+        import os
+        b = BackendId("optimized", worker_count=workers or (os.cpu_count() or 1), tile_size=tile)
+        b.validate()
+        return b
 
     @staticmethod
     def parse(token: str) -> "BackendId":
         if token == "b200":
             return BackendId()
+        if token == "reference":  # backends.cpp:101-111
+            return BackendId.reference()
+        if token == "optimized":
+            return BackendId.optimized()
+        m = re.fullmatch(r"optimized\[tile=(-?\d+)/workers=(-?\d+)\]", token)
+        if m:
+            return BackendId.optimized(int(m.group(2)), int(m.group(1)))
         m = re.fullmatch(r"b200\[device=(\d+)/precision=(fp32|fp64)\]", token)
         if m:
             return BackendId("b200", int(m.group(1)), m.group(2))
         raise ConfigError("unknown backend id: " + token)
+
+
+HOST_KINDS = ("reference", "optimized")
 
 
 # ----------------------------------------------------------------- contexts
@@ -137,6 +178,9 @@ def context(device: int = 0) -> Context:
 
 def _ctx(backend: BackendId) -> Context:
     backend.validate()
+    if backend.is_host:
+        raise ConfigError(f"backend {backend.label()} is a host CPU backend: this library computes only on "
+                          "the B200 (route host backends through estimator.register_host_backend)")
     return context(backend.device)
 
 
@@ -149,6 +193,12 @@ class BackendCapabilities:
 
 
 def capabilities(backend: BackendId) -> BackendCapabilities:
+    backend.validate()
+    if backend.kind == "reference":  # backends.cpp:113-127
+        return BackendCapabilities(backend, True, "scalar triple loop, left-to-right accumulation")
+    if backend.kind == "optimized":
+        return BackendCapabilities(backend, True, f"tiled ({backend.tile_size}x{backend.tile_size}) multi-threaded "
+                                   f"({backend.worker_count} workers), depth-blocked strip accumulation")
     return BackendCapabilities(backend, True, _ctx(backend).describe())
 
 
@@ -324,11 +374,24 @@ def train_device(training, m: int, cfg: KernelConfig = KernelConfig(),
     N, n = training.shape
     if n > 1 and training.stride(1) != N:
         raise ShapeError("train_device: training must be contiguous column-major (ld == N)")
+    _check_device(training, backend, "train_device: training")
+    ctx = _ctx(backend)
+    # the library runs on torch's current stream, so a producer still writing
+    # `training` asynchronously on that stream is ordered before the train
+    ctx.set_stream(torch.cuda.current_stream(training.device).cuda_stream)
     h = C.c_void_p()
-    check(_lib.lib().cs_mset_train_device(_ctx(backend).handle, C.c_void_p(training.data_ptr()), N, n,
-                                          m, int(cfg.kind), cfg._h(), PRECISIONS[backend.precision],
-                                          C.byref(h)))
+    try:
+        check(_lib.lib().cs_mset_train_device(ctx.handle, C.c_void_p(training.data_ptr()), N, n,
+                                              m, int(cfg.kind), cfg._h(), PRECISIONS[backend.precision],
+                                              C.byref(h)))
+    finally:
+        ctx.set_stream(None)
     return TrainedModel(h, backend)
+
+
+def _check_device(t, backend: BackendId, what: str) -> None:
+    if not t.is_cuda or t.device.index != backend.device:
+        raise ConfigError(f"{what} must be a CUDA tensor on device {backend.device} (got {t.device})")
 
 
 def import_model(D, signal_scale, gram_pinv, rank, cfg: KernelConfig,
@@ -396,6 +459,18 @@ def estimate_device(model: TrainedModel, obs, est=None, resid=None, stream=None,
     dtype = {torch.float32: 1, torch.float64: 0}.get(obs.dtype)
     if dtype is None:
         raise ConfigError("estimate_device: observations must be float32 or float64")
+    _check_device(obs, backend, "estimate_device: observations")
+    # outputs are written as N x n values of obs's dtype at obs's leading
+    # dimension: anything else would be written out of bounds or transposed
+    for name, t in (("estimates", est), ("residuals", resid)):
+        if t is None:
+            continue
+        _check_device(t, backend, f"estimate_device: {name}")
+        if t.dtype != obs.dtype or tuple(t.shape) != (N, n) or t.stride(0) != 1 or (n > 1 and t.stride(1) != ld):
+            raise ShapeError(f"estimate_device: {name} must match the observations' dtype, shape and "
+                             f"column-major strides ({obs.dtype}, {(N, n)}, ld={ld})")
+        if t.storage_offset() + (ld * (n - 1) + N if N and n else 0) > t.untyped_storage().nbytes() // t.element_size():
+            raise ShapeError(f"estimate_device: {name} storage is smaller than N x ld")
     ctx = _ctx(backend)
     st = stream if stream is not None else torch.cuda.current_stream(obs.device)
     ctx.set_stream(st.cuda_stream)

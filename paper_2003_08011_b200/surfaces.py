@@ -188,11 +188,24 @@ SURFACE_FORMAT = "containerstress-surface"  # surfaces.cpp:442-443
 
 def backend_to_json(b: BackendId):
     """config.cpp:172-177, extended with the b200 kind."""
+    if b.kind == "reference":
+        return "reference"
+    if b.kind == "optimized":
+        return {"kind": "optimized", "tile_size": b.tile_size, "worker_count": b.worker_count}
     return {"kind": b.kind, "device": b.device, "precision": b.precision}
 
 
 def backend_from_json(j) -> BackendId:
-    if not isinstance(j, dict) or j.get("kind") != "b200":
+    """config.cpp:159-170 (string token or object), plus the b200 kind."""
+    if isinstance(j, str):
+        return BackendId.parse(j)
+    if not isinstance(j, dict):
+        raise ConfigError(f"unknown backend id: {j!r}")
+    if j.get("kind") == "reference":
+        return BackendId.reference()
+    if j.get("kind") == "optimized":
+        return BackendId.optimized(int(j.get("worker_count", 0)), int(j.get("tile_size", 64)))
+    if j.get("kind") != "b200":
         raise ConfigError(f"unknown backend id: {j!r}")
     b = BackendId("b200", int(j["device"]), str(j["precision"]))
     b.validate()

@@ -20,6 +20,7 @@ bracket around synchronous calls (sweep.cpp:212-219), samples clamped to
 """
 from __future__ import annotations
 
+import dataclasses
 import json
 import math
 import os
@@ -186,6 +187,24 @@ def cell_data_seed(master_seed: int, coords: CellCoords, replicate: int) -> int:
     return _seed(master_seed, coords.n_signals, coords.n_observations, coords.n_memory, replicate)
 
 
+def sweep_config_to_json(config: SweepConfig) -> dict:
+    """config.cpp:252-274 (the config echo stored in the surface metadata)."""
+    from .surfaces import backend_to_json
+    kernel = {"kind": KernelKind(config.kernel.kind).name}
+    if config.kernel.bandwidth is not None:
+        kernel["bandwidth"] = config.kernel.bandwidth
+    t = config.signal_template
+    g = config.grid
+    return {"grid": {"signal_counts": list(g.signal_counts), "observation_counts": list(g.observation_counts),
+                     "memory_counts": list(g.memory_counts),
+                     "training_observation_factor": g.training_observation_factor},
+            "replicates": config.replicates, "warmups": config.warmups,
+            "backends": [backend_to_json(b) for b in config.backends], "kernel": kernel,
+            "signals": {"ar_coefficient": t.ar_coefficient, "cross_correlation": t.cross_correlation,
+                        "variance": t.variance, "skewness": t.skewness, "kurtosis": t.kurtosis},
+            "master_seed": config.master_seed, "timer": config.timer, "estimator": config.estimator}
+
+
 def _timer(kind: str) -> Callable[[], float]:
     return time.monotonic if kind == "wall_monotonic" else time.process_time
 
@@ -216,9 +235,11 @@ def _train_eval(coords: CellCoords, config: SweepConfig, backend: BackendId, tra
     import torch
     from .estimator import MsetModel, algorithm_by_name
     from .mset import estimate_device, train_device
-    if config.estimator != "mset2":
+    if config.estimator != "mset2" or backend.is_host:
+        # host backends (and the non-GPU estimators) take host FP64 copies of
+        # the replicate's signals, made outside the timed brackets
         algo = algorithm_by_name(config.estimator)
-        X, O = training.cpu().numpy(), surveil.cpu().numpy()
+        X, O = training.double().cpu().numpy(), surveil.double().cpu().numpy()
         t0 = clock()
         model = algo.train(X, coords.n_memory, config.kernel, backend)
         t1 = clock()
@@ -250,7 +271,7 @@ def run_unit(coords: CellCoords, replicate: int, config: SweepConfig, device: in
     rec = {"coords": (coords.n_signals, coords.n_observations, coords.n_memory),
            "replicate": replicate, "seed": cell_data_seed(config.master_seed, coords, replicate),
            "train": [], "surveil": [], "error": None, "error_kind": None}
-    backends = [BackendId(b.kind, device, b.precision) for b in config.backends]
+    backends = [b if b.is_host else dataclasses.replace(b, device=device) for b in config.backends]
     try:
         if warm:
             for w in range(config.warmups):
@@ -346,13 +367,24 @@ def run_sweep(config: SweepConfig, progress: Optional[Callable] = None, *, world
     mine = plan_units(units, world)[rank]
     records = []
     seen = set()
-    for idx, coords, r in mine:
-        warm = idx not in seen  # one warm-up pass per (cell, rank), as run_cell does per cell
-        seen.add(idx)
-        rec = unit_runner(coords, r, config, device, warm)
-        rec["cell_index"] = idx
-        records.append(rec)
+    fatal = None
+    try:
+        for idx, coords, r in mine:
+            warm = idx not in seen  # one warm-up pass per (cell, rank), as run_cell does per cell
+            seen.add(idx)
+            rec = unit_runner(coords, r, config, device, warm)
+            rec["cell_index"] = idx
+            records.append(rec)
+    except Exception as e:  # noqa: BLE001 -- every rank must still reach the gather
+        fatal = f"rank {rank}: {type(e).__name__}: {e}"
+        records = [{"fatal": fatal}]
     gathered = _gather(records, world)
+    # a non-Error failure (e.g. CUDA OOM) aborts the sweep as the serial
+    # reference would -- on every rank, after the gather, so no rank is left
+    # waiting in the collective
+    fatals = [rec["fatal"] for part in gathered for rec in part if "fatal" in rec]
+    if fatals:
+        raise RuntimeError("run_sweep aborted: " + "; ".join(fatals))
     if rank != 0:
         return None
     by_cell = {}
@@ -375,13 +407,14 @@ def run_sweep(config: SweepConfig, progress: Optional[Callable] = None, *, world
         "hardware_threads": os.cpu_count(),
         "timer": config.timer,
         "rng_algorithm": RNG_ALGORITHM,
+        "config": sweep_config_to_json(config),
         "world_size": world,
         "placement": "LPT over (cell, replicate) units; records gathered with torch.distributed",
         "started_at": started,
         "finished_at": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
     }
     try:
-        meta["backend_capabilities"] = [capabilities(BackendId(b.kind, device, b.precision)).description
+        meta["backend_capabilities"] = [capabilities(b if b.is_host else dataclasses.replace(b, device=device)).description
                                         for b in config.backends]
     except errors.Error:
         meta["backend_capabilities"] = []

@@ -127,3 +127,31 @@ def test_sweep_surface_files_and_speedup(p, tmp_path):
     assert len(holes) == 2 and all(c.reason == "m<2n" for c in holes)  # (8, 2000, 8) train + surveil
     assert all(c.speedup > 0 for c in sp.cells if not c.hole)
     export_speedup_csv(sp, Phase.surveil, str(tmp_path / "sp.csv"))
+
+
+def test_sweep_gpu_vs_host_speedup_surface(p, tmp_path):
+    # sweep.cpp:206-227: every backend of a replicate runs inside one
+    # run_cell, so host and GPU cells share the surface and speedup()
+    # (surfaces.cpp:100-145) gives the GPU-vs-host ratio directly.  The host
+    # backend is the CPU oracle registered as the reference's "optimized"
+    # kind (baseline leg; the library itself never computes on the CPU).
+    from oracle import host_backend
+    from paper_2003_08011_b200 import BackendId
+    from paper_2003_08011_b200.surfaces import export_speedup_csv, export_surface_json, import_surface_json, speedup
+    from paper_2003_08011_b200.sweep import Phase, SweepConfig, SweepGrid, run_sweep
+    host_backend.register()
+    try:
+        cpu, gpu = BackendId.optimized(4, 64), BackendId("b200", 0, "fp32")
+        cfg = SweepConfig(SweepGrid([10, 20], [2000], [40, 100]), replicates=2, warmups=1,
+                          master_seed=20260810, backends=[cpu, gpu])
+        s = run_sweep(cfg)
+        assert len(s.cells) == 4 * 2 * 2
+        assert not any(c.excluded for c in s.cells)
+        sp = speedup(s, cpu, gpu)
+        assert all(c.speedup > 1.0 for c in sp.cells if not c.hole)
+        export_speedup_csv(sp, Phase.surveil, str(tmp_path / "sp.csv"))
+        export_surface_json(s, str(tmp_path / "s.json"))
+        back = import_surface_json(str(tmp_path / "s.json"))
+        assert {c.backend for c in back.cells} == {cpu, gpu}
+    finally:
+        host_backend.unregister()

@@ -134,3 +134,90 @@ def test_two_rank_gloo_sweep_matches_single_rank():
     reasons = {r for *_, ex, r in got if ex}
     assert reasons == {"m<2n", "no real Fleishman solution"}
     assert len(got) == 18 * 2  # 18 grid cells x 2 phases x 1 backend
+
+
+# ------------------------------------------------------- host backend kinds
+def test_backend_id_label_parse_validate():
+    # test_backends.cpp:159-171 plus the b200 kind
+    from paper_2003_08011_b200 import BackendId
+    assert BackendId.reference().label() == "reference"
+    o = BackendId.optimized(4, 32)
+    assert o.label() == "optimized[tile=32/workers=4]"
+    assert BackendId.parse(o.label()) == o
+    assert BackendId.parse("reference") == BackendId.reference()
+    assert BackendId.parse("b200[device=1/precision=fp32]") == BackendId("b200", 1, "fp32")
+    for bad in ("optimized[tile=4/workers=2]", "optimized[tile=64/workers=-1]", "gpu"):
+        with pytest.raises(errors.ConfigError):
+            BackendId.parse(bad)
+    from paper_2003_08011_b200.surfaces import backend_from_json, backend_to_json
+    for b in (BackendId.reference(), o, BackendId("b200", 0, "fp64")):
+        assert backend_from_json(backend_to_json(b)) == b
+
+
+def test_host_backend_requires_registration_and_matches_oracle(oracle):
+    import numpy as np
+    from oracle import host_backend
+    from paper_2003_08011_b200 import BackendId, KernelConfig, algorithm_by_name
+    algo = algorithm_by_name("mset2")
+    X = oracle.synthesize_uniform(4, 80, 0.5, 0.3, 1.0, 0.5, 4.0, 7)
+    obs = oracle.synthesize_uniform(4, 50, 0.5, 0.3, 1.0, 0.5, 4.0, 8)
+    host_backend.unregister()
+    with pytest.raises(errors.ConfigError):
+        algo.train(X, 20, KernelConfig(), BackendId.optimized(2))
+    host_backend.register()
+    try:
+        for b in (BackendId.reference(), BackendId.optimized(2, 16)):
+            model = algo.train(X, 20, KernelConfig(), b)
+            r = algo.estimate(model, obs, b)
+            ref = oracle.train(X, 20)
+            want_e, want_r = oracle.estimate(ref, obs)
+            assert np.abs(r.estimates - want_e).max() <= 1e-10 * np.abs(want_e).max()
+            assert np.array_equal(r.residuals, obs - r.estimates)
+        # a host model on the b200 backend (and vice versa) is a ConfigError
+        # (estimator.cpp:17-23)
+        with pytest.raises(errors.ConfigError):
+            algo.estimate(model, obs, BackendId("b200", 0, "fp64"))
+    finally:
+        host_backend.unregister()
+
+
+def test_sweep_config_echo_in_metadata():
+    from paper_2003_08011_b200.sweep import sweep_config_to_json
+    s = run_sweep(_sweep_config(), unit_runner=_fake_unit)
+    echo = s.metadata["config"]
+    assert echo == sweep_config_to_json(_sweep_config())
+    assert echo["grid"]["memory_counts"] == [2, 4, 8] and echo["replicates"] == 3
+    assert echo["backends"] == [{"kind": "b200", "device": 0, "precision": "fp32"}]
+
+
+def _boom_unit(coords, replicate, config, device, warm):
+    import torch.distributed as dist
+    if dist.get_rank() == 1:
+        raise MemoryError("simulated device OOM")
+    return _fake_unit(coords, replicate, config, device, warm)
+
+
+def _fatal_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        run_sweep(_sweep_config(), world=world, rank=rank, unit_runner=_boom_unit)
+        q.put((rank, "returned"))
+    except RuntimeError as e:
+        q.put((rank, str(e)))
+    dist.destroy_process_group()
+
+
+def test_non_error_failure_aborts_every_rank_without_hanging():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fatal_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert set(got) == {0, 1}
+    assert all("simulated device OOM" in v for v in got.values()), got

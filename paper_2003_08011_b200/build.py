@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcstress_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["cstress_b200.cu", "synth.cpp", "model_io.cpp"]
+SOURCES = ["cstress_b200.cu", "train_f64.cu", "synth.cpp", "model_io.cpp"]
 
 
 def _sources():
@@ -39,15 +39,47 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
+OBJ_DIR = os.path.join(HERE, "build")
+
+
+def _obj(src):
+    return os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+
+
+def _obj_stale(src) -> bool:
+    """An object is stale when its source or any header it included (the
+    nvcc -MD dependency file) is newer, or this build script changed."""
+    o, d = _obj(src), _obj(src) + ".d"
+    if not (os.path.exists(o) and os.path.exists(d)):
+        return True
+    t = os.path.getmtime(o)
+    deps = [src, os.path.abspath(__file__)]
+    text = open(d).read().replace("\\\n", " ")
+    for tok in text.split(":", 1)[-1].split():
+        deps.append(tok)
+    return any((not os.path.exists(p)) or os.path.getmtime(p) > t for p in deps)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each source to an object (in parallel, incrementally via the
+    -MD dependency files) and link libcstress_b200.so."""
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *_sources(), "-o", LIB + ".tmp",
-           "-lpthread", "-ldl"]
-    subprocess.run(cmd, check=True, cwd=CSRC)
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v" if verbose else "-O3",
+              "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    todo = [s for s in _sources() if force or _obj_stale(s)]
+
+    def compile_one(src):
+        subprocess.run([*common, "-MD", "-MF", _obj(src) + ".d", "-c", src, "-o", _obj(src)], check=True, cwd=CSRC)
+
+    with ThreadPoolExecutor(max_workers=max(1, len(todo))) as ex:
+        for f in [ex.submit(compile_one, s) for s in todo]:
+            f.result()
+    subprocess.run([NVCC, *ARCH, "--shared", "-Xcompiler", "-fPIC", *[_obj(s) for s in _sources()],
+                    "-o", LIB + ".tmp", "-lpthread", "-ldl"], check=True, cwd=CSRC)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -32,6 +32,7 @@
 #include "selection.cuh"
 #include "solver.cuh"
 #include "synth.cuh"
+#include "train_f64.h"
 
 using namespace csb;
 
@@ -411,29 +412,22 @@ bool tri_inverse_product(cs_ctx* ctx, const double* L, int64_t m, double* out) {
 
 // Gram matrix of a model's normalised memory vectors (mset.cpp:151-152).
 // FP64-precision models: `sim_exact`, the reference's loop order bit for bit.
-// FP32-precision models (tolerance contract) at m >= 512: S = D_norm^T D_norm
-// as a cuBLAS DGEMM on the FP64 tensor-core path, then the kernel map of
-// ||d_i||^2 + ||d_j||^2 - 2 S_ij (2 n m^2 flops at DGEMM rate instead of
-// 3 n m^2 on CUDA cores; C3: 3.2 -> 1.2 ms).  Deterministic, so the lazy
-// eigen_spectrum re-forms the identical matrix.  CSB_GRAM_EXACT=1 forces the
-// exact kernel for every model.
+// FP32-precision models (tolerance contract): the DMMA Gram of train_f64.cu
+// -- D_norm^T D_norm on the FP64 tensor pipe (lower triangle, mirrored) with
+// the kernel map of ||d_i||^2 + ||d_j||^2 - 2 S_ij, the exact unit diagonal
+// and the direct-difference recompute of cancellation-prone entries fused in
+// the epilogue (duplicate / near-duplicate memory vectors get the
+// reference's values, so the rank decision matches the exact Gram).
+// Deterministic, so the lazy eigen_spectrum re-forms the identical matrix.
+// CSB_GRAM_EXACT=1 forces the exact kernel for every model.
 void form_gram(cs_ctx* ctx, const cs_model* M, double* gram) {
   cudaStream_t st = ctx->stream;
   const int64_t n = M->n, m = M->m;
   const char* env = std::getenv("CSB_GRAM_EXACT");
-  const bool exact = (env && env[0] == '1') || M->precision != CS_PRECISION_FP32 || m < 512;
-  if (!exact && cublas_handle(ctx)) {
-    TmpBuf<double> dd(m);
-    col_sqnorm_kernel<<<ceil_div(m, 128), 128, 0, st>>>(M->Dn.get(), n, m, dd.get());
-    CSB_LAUNCH_CHECK();
-    const double one = 1.0, zero = 0.0;
-    if (cublas_api().dgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(m), static_cast<int>(m),
-                           static_cast<int>(n), &one, M->Dn.get(), static_cast<int>(n), M->Dn.get(),
-                           static_cast<int>(n), &zero, gram, static_cast<int>(m)) == CUBLAS_STATUS_SUCCESS) {
-      gram_from_dot_kernel<<<grid_for(m * m), 256, 0, st>>>(gram, dd.get(), m, M->kind, M->h);
-      CSB_LAUNCH_CHECK();
-      return;
-    }
+  const bool exact = (env && env[0] == '1') || M->precision != CS_PRECISION_FP32;
+  if (!exact) {
+    dmma_gram(st, M->Dn.get(), n, m, M->kind, M->h, gram);
+    return;
   }
   launch_sim_exact(st, M->Dn.get(), n, M->Dn.get(), n, n, m, m, M->kind, M->h, gram, m);
 }
@@ -441,16 +435,20 @@ void form_gram(cs_ctx* ctx, const cs_model* M, double* gram) {
 // Full-rank fast path of the pseudo-inverse: when every eigenvalue passes the
 // reference cutoff (rank == m), G+ = V L^-1 V^T = G^-1 exactly, computed here
 // by Cholesky factorisation + inverse (~m^3 flops instead of syevd's vector
-// phase and the W W^T product).  Returns false when G is not numerically
-// positive definite, in which case the caller takes the eigenvector path.
+// phase and the W W^T product).  Default: the own recursive blocked
+// factorisation on the DMMA tensor pipe (train_f64.cu).  CSB_POTRI=1|2|3
+// select the round-1 cuSOLVER routes (potri / potrs / potrf + cuBLAS
+// recursion) for A/B runs.  Returns false when G is not numerically positive
+// definite, in which case the caller takes the eigenvector path.
 bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
   cudaStream_t st = ctx->stream;
+  const int mi = static_cast<int>(m);
+  const char* env = std::getenv("CSB_POTRI");
+  if (!(env && (env[0] == '1' || env[0] == '2' || env[0] == '3'))) return dmma_chol_inverse(st, G, m, out);
   const CusolverApi& api = cusolver_api();
   if (!ctx->solver) solver_check(api.create(&ctx->solver), "cusolverDnCreate");
   solver_check(api.set_stream(ctx->solver, st), "SetStream");
-  const int mi = static_cast<int>(m);
-  const char* env = std::getenv("CSB_POTRI");
-  if (env && env[0] == '1') {
+  if (env[0] == '1') {
     // factor + potri (triangular inverse and L^-T L^-1 in place)
     CSB_CUDA(cudaMemcpyAsync(out, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
     int l1 = 0, l2 = 0;
@@ -466,12 +464,10 @@ bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
     CSB_CUDA(cudaMemcpyAsync(h, info.get(), sizeof h, cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaStreamSynchronize(st));
     if (h[0] != 0 || h[1] != 0) return false;
-  } else {
-    // factor, then G^-1 = L^-T L^-1 by the blocked DGEMM recursion
-    // (tri_inverse_product), or potrs(L, I) -- two triangular solves with m
-    // right-hand sides -- where cuBLAS is absent or CSB_POTRI=2; the in-place
-    // potri (trtri + lauum) was ~8x slower at m = 1000-4000, and cuSOLVER
-    // Xtrtri + DSYRK 40% slower than potrs at m = 2000-4000
+  } else if (env && (env[0] == '2' || env[0] == '3')) {
+    // factor, then G^-1 = L^-T L^-1 by the blocked cuBLAS DGEMM recursion
+    // (CSB_POTRI=3), or potrs(L, I) (CSB_POTRI=2) -- the round-1 routes, kept
+    // for A/B runs
     TmpBuf<double> L(static_cast<size_t>(m) * m);
     CSB_CUDA(cudaMemcpyAsync(L.get(), G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
     int l1 = 0;
@@ -485,7 +481,7 @@ bool cholesky_inverse(cs_ctx* ctx, const double* G, int64_t m, double* out) {
     CSB_CUDA(cudaMemcpyAsync(&hf, info.get(), sizeof hf, cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaStreamSynchronize(st));
     if (hf != 0) return false;  // not numerically positive definite
-    const bool blocked = !(env && env[0] == '2') && tri_inverse_product(ctx, L.get(), m, out);
+    const bool blocked = env[0] == '3' && tri_inverse_product(ctx, L.get(), m, out);
     if (!blocked) {
       set_identity_kernel<<<grid_for(m * m), 256, 0, st>>>(out, m);
       CSB_LAUNCH_CHECK();
@@ -607,13 +603,8 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
   // per-signal power-of-two scales
   TmpBuf<double> P(static_cast<size_t>(n) * m);
   // P carries no reference association (the reference forms W = G+ S, then
-  // D W): a plain library DGEMM on the FP64 tensor-core path (C3 shape:
-  // 3.4 -> 2.1 ms packing), the exact-order kernel where cuBLAS is absent
-  const double one = 1.0, zero = 0.0;
-  if (!cublas_handle(ctx) ||
-      cublas_api().dgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, m, m, &one, M->Dn.get(), n, M->pinv.get(), m,
-                         &zero, P.get(), n) != CUBLAS_STATUS_SUCCESS)
-    launch_gemm_exact<false, false>(st, M->Dn.get(), n, M->pinv.get(), m, n, m, m, P.get(), n);
+  // D W): the DMMA GEMM of train_f64.cu on the FP64 tensor pipe
+  dmma_gemm(st, 0, n, m, m, 1.0, M->Dn.get(), n, M->pinv.get(), m, 0.0, P.get(), n);
   M->p_shift.resize(n);
   M->scale_out_d.resize(n);
   M->scale_out_f.resize(n);

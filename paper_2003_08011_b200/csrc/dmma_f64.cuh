@@ -1,13 +1,14 @@
 // dmma_f64.cuh -- FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) kernels of
-// the train path: a grouped GEMM with triangle-aware K clipping and two
-// epilogues (plain alpha/beta, and the Gram similarity map), and the
-// single-CTA Cholesky + triangular-inverse leaf of the recursive
-// factorisation in train_f64.cu.
+// the train path (train_f64.cu): a grouped GEMM with triangle-aware K
+// clipping and two epilogues (alpha/beta, and the Gram similarity map), and
+// the single-CTA Cholesky + triangular-inverse leaf of the recursive
+// factorisation.
 //
 // The reference's train arithmetic is FP64 throughout (types.hpp:13); B200
-// has no tcgen05 f64 kind, so the FP64 tensor path is the legacy DMMA
-// instruction (SASS `DMMA.884`).  Fragment layout of m8n8k4 (.row.col):
-// lane l = 4 g + t holds A[g][t], B[t][g] and C[g][2t .. 2t+1].
+// has no tcgen05 f64 kind, so the FP64 tensor path is the DMMA instruction
+// (SASS `DMMA.884`, 37 TFLOP/s measured, profiles/peaks_probe.json).
+// Fragment layout of m8n8k4 (.row.col): lane l = 4 g + t holds A[g][t],
+// B[t][g] and C[g][2t .. 2t+1].
 #pragma once
 
 #include <cuda_runtime.h>
@@ -17,9 +18,9 @@
 namespace csb {
 
 // ------------------------------------------------------------------ GEMM
-// One product C = alpha op(A) op(B) + beta C of a grouped launch.
-// op(A) is M x K, op(B) is K x N, C is M x N, all column-major.
-// Flags describe zero structure of the (logical) operands so a tile skips
+// One product C = alpha op(A) op(B) + beta C of a grouped launch; op(A) is
+// M x K, op(B) is K x N, C is M x N, all column-major.  Flags give the
+// transposes and the zero structure of the logical operands, so a tile skips
 // the K range that cannot contribute, and which output tiles to compute.
 enum DgemmFlags : int {
   kALower = 1,    // op(A)(i, k) == 0 for k > i
@@ -28,6 +29,9 @@ enum DgemmFlags : int {
   kBUpper = 8,    // op(B)(k, j) == 0 for k > j
   kCLower = 16,   // compute only the lower triangle (i >= j); requires M == N
   kCMirror = 32,  // with kCLower: also write C(j, i) = C(i, j) (symmetric output)
+  kTransA = 64,   // op(A) = A^T (A stored K x M)
+  kTransB = 128,  // op(B) = B^T (B stored N x K)
+  kReverse = 256, // enumerate tiles in reverse (heaviest K ranges first under kALower / kBUpper)
 };
 
 struct DgemmProblem {
@@ -38,10 +42,11 @@ struct DgemmProblem {
   int M, N, K;
   int flags;
   double alpha, beta;
-  int tiles_m, tiles;  // output tiles of this problem (filled by the host)
+  int tiles_m, pad_;
 };
 
-constexpr int kDgemmMaxGroup = 16;
+// small: the group is a kernel parameter, copied into every launch
+constexpr int kDgemmMaxGroup = 4;
 
 struct DgemmGroup {
   DgemmProblem p[kDgemmMaxGroup];
@@ -49,12 +54,13 @@ struct DgemmGroup {
   int tile_start[kDgemmMaxGroup + 1];
 };
 
-// Gram epilogue (mset.cpp:151-152 via the GEMM form ||a||^2+||b||^2-2a.b):
-// G(i, j) = k(d2), exact 1 on the diagonal (d2(x, x) = 0 exactly in the
-// reference), and entries whose GEMM-form d2 is small relative to the norms
-// (d2 < tau (dd_i + dd_j), where cancellation would dominate -- SURVEY H2)
-// recomputed by direct differences in the reference's order
-// (backends.cpp:139-150).
+// Gram epilogue (mset.cpp:151-152 through the GEMM form ||a||^2 + ||b||^2 -
+// 2 a.b): G(i, j) = k(d2) with the exact 1 on the diagonal (d2(x, x) = 0
+// exactly in the reference), and any entry whose GEMM-form d2 is small
+// relative to the norms (d2 < tau (dd_i + dd_j), where cancellation would
+// dominate -- SURVEY H2) recomputed by direct differences in the reference's
+// order (backends.cpp:139-150), so duplicate and near-duplicate memory
+// vectors get the reference's values.
 struct GramEpi {
   const double* Dn;  // n x m column-major (normalised memory vectors)
   const double* dd;  // ||Dn(:, i)||^2
@@ -77,6 +83,10 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
   const int sz = valid ? 8 : 0;  // src-size 0: zero fill
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(src), "r"(sz) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -92,31 +102,37 @@ __device__ __forceinline__ double kernel_from_d2(double d2, int kind, double h) 
 }  // namespace dmma
 
 // Tile shape: BM x BN output per CTA, BK-deep shared-memory stages, warps of
-// WM x WN.  Shared rows are padded by 8 doubles so a fragment load (4 k-rows
-// x 8 consecutive i) touches all 32 banks twice (2 wavefronts, the minimum
-// for 256 bytes).
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+// WM x WN.  Shared rows are padded to a stride of 4 (mod 16) doubles: a
+// 64-bit fragment load is served per half-warp (lanes g = 0..3 or 4..7,
+// t = 0..3 reading k-row t, column g), and with that stride the 16 doubles of
+// a half-warp land on 16 distinct bank pairs -- 2 wavefronts per load, the
+// minimum.  (A stride of 8 mod 16 put k-rows t and t + 2 on the same banks:
+// ncu measured 4.1-way conflicts and an L1-bound GEMM.)
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
 struct DgemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
   static constexpr int kWarps = (BM / WM) * (BN / WN);
   static constexpr int kThreads = kWarps * 32;
-  static constexpr int kPadA = BM + 8, kPadB = BN + 8;
+  static constexpr int kPadA = BM + 4, kPadB = BN + 4;
   static constexpr int kStageDoubles = BK * (kPadA + kPadB);
   static constexpr size_t kSmem = sizeof(double) * STAGES * kStageDoubles;
   static constexpr int MI = WM / 8, NI = WN / 8;
 };
 
-// Grouped FP64 GEMM.  TA: op(A) = A^T (A stored K x M); TB: op(B) = B^T.
-// EPI 0: C = alpha acc + beta C.  EPI 1: Gram map (GramEpi), problem 0 only.
-template <class Cfg, int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB, int EPI>
+// Grouped FP64 GEMM.  EPI 0: C = alpha acc + beta C.  EPI 1: Gram map
+// (GramEpi) for every problem of the group.
+template <class Cfg, int EPI>
 __global__ void __launch_bounds__(Cfg::kThreads)
 dgemm_dmma_kernel(const __grid_constant__ DgemmGroup grp, const __grid_constant__ GramEpi gram) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   extern __shared__ __align__(16) double smem[];
   // ---- which problem / tile
   int pi = 0;
   const int bid = blockIdx.x;
   while (pi + 1 < grp.count && bid >= grp.tile_start[pi + 1]) ++pi;
   const DgemmProblem& P = grp.p[pi];
-  int t = bid - grp.tile_start[pi];
+  const int nt = grp.tile_start[pi + 1] - grp.tile_start[pi];
+  const int t = (P.flags & kReverse) ? nt - 1 - (bid - grp.tile_start[pi]) : bid - grp.tile_start[pi];
   int bm, bn;
   if (P.flags & kCLower) {
     // lower-triangle tile enumeration: t -> (bm >= bn)
@@ -137,9 +153,10 @@ dgemm_dmma_kernel(const __grid_constant__ DgemmGroup grp, const __grid_constant_
   if (P.flags & kBLower) k_lo = max(k_lo, j0);
   k_lo = (k_lo / BK) * BK;
   const int ktiles = k_hi > k_lo ? (k_hi - k_lo + BK - 1) / BK : 0;
+  const bool ta = P.flags & kTransA, tb = P.flags & kTransB;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp % (BM / WM)) * WM, wn0 = (warp / (BM / WM)) * WN;
+  const int wm0 = (warp % (BM / Cfg::WM)) * Cfg::WM, wn0 = (warp / (BM / Cfg::WM)) * Cfg::WN;
   const int g = lane >> 2, tq = lane & 3;
 
   const double* __restrict__ A = P.A;
@@ -147,24 +164,27 @@ dgemm_dmma_kernel(const __grid_constant__ DgemmGroup grp, const __grid_constant_
   auto As = [&](int s) { return smem + s * Cfg::kStageDoubles; };
   auto Bs = [&](int s) { return smem + s * Cfg::kStageDoubles + BK * Cfg::kPadA; };
 
+  // stage loads: element (i, k) of op(A) goes to as[k * kPadA + i]; the
+  // thread -> element map walks the contiguous dimension of the stored
+  // operand so global reads coalesce
   auto load_stage = [&](int s, int kt) {
     const int kb = k_lo + kt * BK;
     double* as = As(s);
     double* bs = Bs(s);
     for (int e = tid; e < BM * BK; e += Cfg::kThreads) {
       int i, k;
-      if (TA) { k = e % BK; i = e / BK; } else { i = e % BM; k = e / BM; }
+      if (ta) { k = e % BK; i = e / BK; } else { i = e % BM; k = e / BM; }
       const int gi = i0 + i, gk = kb + k;
       const bool ok = gi < P.M && gk < k_hi;
-      const double* src = TA ? A + (static_cast<int64_t>(gi) * P.lda + gk) : A + (gi + static_cast<int64_t>(gk) * P.lda);
+      const double* src = ta ? A + (static_cast<int64_t>(gi) * P.lda + gk) : A + (gi + static_cast<int64_t>(gk) * P.lda);
       dmma::cp_async8(as + k * Cfg::kPadA + i, ok ? src : A, ok);
     }
     for (int e = tid; e < BN * BK; e += Cfg::kThreads) {
       int j, k;
-      if (TB) { j = e % BN; k = e / BN; } else { k = e % BK; j = e / BK; }
+      if (tb) { j = e % BN; k = e / BN; } else { k = e % BK; j = e / BK; }
       const int gj = j0 + j, gk = kb + k;
       const bool ok = gj < P.N && gk < k_hi;
-      const double* src = TB ? B + (gj + static_cast<int64_t>(gk) * P.ldb) : B + (gk + static_cast<int64_t>(gj) * P.ldb);
+      const double* src = tb ? B + (gj + static_cast<int64_t>(gk) * P.ldb) : B + (gk + static_cast<int64_t>(gj) * P.ldb);
       dmma::cp_async8(bs + k * Cfg::kPadB + j, ok ? src : B, ok);
     }
   };
@@ -247,69 +267,261 @@ dgemm_dmma_kernel(const __grid_constant__ DgemmGroup grp, const __grid_constant_
 }
 
 // ------------------------------------------------------ Cholesky leaf
-// Factor the b x b (b <= kLeaf) diagonal block at (r0, r0) of the
-// lower-triangular work matrix L (ld m) in shared memory, G_bb = L_bb L_bb^T,
-// then invert L_bb in place (column by column from the right,
-// X(j+1:, j) = -X(j+1:, j+1:) L(j+1:, j) / L(j, j)), and write X_bb = L_bb^-1
-// into X.  A non-positive or non-finite pivot sets *fail (the caller then
-// takes the reference's eigen route).  One CTA of kLeafThreads.
+// One CTA factors the b x b (b <= kLeaf) diagonal block at (r0, r0) of A
+// (lower triangle read, ld lda), A_bb = L L^T, and writes X_bb = L^-1 (lower)
+// into X.  Blocked by 32 inside the CTA:
+//   factor:  for each 32-column block k: one warp factors L_kk in registers
+//            (shuffle broadcasts; one reciprocal square root per pivot, no
+//            FP64 division on the chain) and inverts it column-parallel
+//            (X_kk, kept in place of L_kk); the panel below becomes
+//            L_ik = A_ik X_kk^T and the trailing lower triangle takes the
+//            rank-32 update A_ij -= L_ik L_jk^T -- both as warp-level DMMA
+//            products over 16 x 16 output quadrants;
+//   inverse: X_IJ = -X_II (sum_{K=J..I-1} L_IK X_KJ) by block distance
+//            I - J = 1, 2, 3 (DMMA quadrants again); the diagonal X blocks
+//            replace L's, the off-diagonal ones go to a second buffer.
+// Column stride kLeafLd = 132 (4 mod 16): DMMA fragment loads are 2
+// wavefronts (see DgemmCfg).  Padding rows / columns (b .. 32 nb) are the
+// identity.  A non-positive or non-finite pivot sets *fail (the caller then
+// takes the reference's eigen route).
 constexpr int kLeaf = 128;
-constexpr int kLeafThreads = 512;
-constexpr int kLeafLd = kLeaf;  // column stride 129 doubles in the trailing update: conflict-free
+constexpr int kLeafThreads = 256;
+constexpr int kLeafLd = 132;
+constexpr int kLeafTLd = 36;
+// S (the factor, 128 x 132) + Tm (3 pair products) + Xo (6 off-diagonal X blocks)
+constexpr size_t kLeafSmem = sizeof(double) * (kLeaf * kLeafLd + 9 * 32 * kLeafTLd);
+#ifdef CSB_LEAF_PROFILE
+__device__ long long g_leaf_clk[64];
+#define LEAF_MARK(slot) \
+  if (threadIdx.x == 0) g_leaf_clk[slot] = clock64();
+#else
+#define LEAF_MARK(slot)
+#endif
+
+namespace dmma {
+// 16 x 16 output quadrant of a warp: acc[a][b] is the m8n8 subtile (8a.., 8b..);
+// lane (g, t) holds rows 8a + g, columns 8b + 2t, 8b + 2t + 1
+template <class FA, class FB>
+__device__ __forceinline__ void warp_mma16(double (&acc)[2][2][2], int K, FA a_at, FB b_at, int g, int t) {
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const double a0 = a_at(g, k0 + t), a1 = a_at(8 + g, k0 + t);
+    const double b0 = b_at(k0 + t, g), b1 = b_at(k0 + t, 8 + g);
+    mma884(acc[0][0], a0, b0);
+    mma884(acc[0][1], a0, b1);
+    mma884(acc[1][0], a1, b0);
+    mma884(acc[1][1], a1, b1);
+  }
+}
+}  // namespace dmma
 
 __global__ void __launch_bounds__(kLeafThreads)
-chol_leaf_kernel(const double* __restrict__ L, int64_t m, int64_t r0, int b, double* __restrict__ X,
-                 int* __restrict__ fail) {
-  extern __shared__ double S[];  // [kLeaf cols][kLeafLd] column-major, + kLeaf temp
-  double* col = S + kLeaf * kLeafLd;
-  __shared__ int bad;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  for (int e = tid; e < b * b; e += kLeafThreads) {
-    const int i = e % b, j = e / b;
-    S[j * kLeafLd + i] = i >= j ? L[(r0 + i) + (r0 + j) * m] : 0.0;
+chol_inv_leaf_kernel(const double* __restrict__ A, int64_t lda, int64_t r0, int b, double* __restrict__ X,
+                     int64_t ldx, int* __restrict__ fail) {
+  extern __shared__ __align__(16) double S[];  // [kLeaf cols][kLeafLd]
+  double* Tm = S + kLeaf * kLeafLd;            // [3][32 cols][kLeafTLd] products of the inverse phase
+  double* Xo = Tm + 3 * 32 * kLeafTLd;         // [6][32 cols][kLeafTLd] X_IJ, I > J (column-major)
+  LEAF_MARK(0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  constexpr int kWarps = kLeafThreads / 32;
+  const int nb = (b + 31) / 32, bp = nb * 32;
+  auto at = [&](int i, int j) -> double& { return S[j * kLeafLd + i]; };
+  // X_IJ (I > J) lives in Xo, block index I (I - 1) / 2 + J
+  auto xo = [&](int I, int J) -> double* { return Xo + (I * (I - 1) / 2 + J) * 32 * kLeafTLd; };
+  // load: the bp x bp block by cp.async (16-byte copies of row pairs when
+  // lda is even), then zero the diagonal blocks' upper parts and put the
+  // identity on the padding
+  if ((lda & 1) == 0 && (b & 1) == 0) {
+    for (int j = warp; j < bp; j += kLeafThreads / 32)
+      for (int i = 2 * lane; i < bp; i += 64) {
+        if (i < b && j < b) dmma::cp_async16(&at(i, j), A + (r0 + i) + (r0 + j) * lda);
+        else at(i, j) = at(i + 1, j) = 0.0;
+      }
+  } else {
+    for (int j = warp; j < bp; j += kLeafThreads / 32)
+      for (int i = lane; i < bp; i += 32) {
+        const bool ok = i < b && j < b;
+        dmma::cp_async8(&at(i, j), ok ? A + (r0 + i) + (r0 + j) * lda : A, ok);
+      }
   }
+  dmma::cp_commit();
+  dmma::cp_wait<0>();
   __syncthreads();
-  // right-looking Cholesky: thread (jc, q) owns column jc, rows i = q (mod 4)
-  const int jc = tid % kLeaf, q = tid / kLeaf;
-  for (int k = 0; k < b; ++k) {
-    if (tid == 0) {
-      const double d = S[k * kLeafLd + k];
-      if (!(d > 0.0) || !isfinite(d)) bad = 1;
-      S[k * kLeafLd + k] = sqrt(fmax(d, 0.0));
+  for (int e = tid; e < nb * 1024; e += kLeafThreads) {
+    const int blk = e >> 10, i = (e >> 5) & 31, j = e & 31;
+    if (i < j) at(32 * blk + i, 32 * blk + j) = 0.0;
+  }
+  for (int i = b + tid; i < bp; i += kLeafThreads) at(i, i) = 1.0;
+  __syncthreads();
+  LEAF_MARK(1);
+  int bad = 0;
+  for (int kb = 0; kb < nb; ++kb) {
+    const int c0 = 32 * kb;
+    if (warp == 0) {
+      // L_kk: lane i holds row i of the block
+      double r[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) r[k] = k <= lane ? at(c0 + lane, c0 + k) : 0.0;
+      // the pivot chain: rsqrt -> scale -> the next diagonal on its own lane
+      // -> one shuffle; the other lanes' updates hang off the chain
+      // (column j of L is broadcast through shared memory: one store per
+      // lane and broadcast loads, half the instructions of 64-bit shuffles)
+      double* lc = Tm;  // [2][32], free until the inverse phase
+      double piv = __shfl_sync(0xffffffffu, r[0], 0);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (!(piv > 0.0) || !isfinite(piv)) bad = 1;
+        const double inv = rsqrt(fmax(piv, 1e-300));
+        const double lj = lane == j ? piv * inv : (lane > j ? r[j] * inv : 0.0);
+        r[j] = lj;
+        if (j < 31) {
+          lc[(j & 1) * 32 + lane] = lj;
+          const double dnext = fma(-lj, lj, r[j + 1]);  // lane j + 1: its diagonal after step j
+          piv = __shfl_sync(0xffffffffu, dnext, j + 1);
+          __syncwarp();
+#pragma unroll
+          for (int k = j + 1; k < 32; ++k) r[k] = fma(-lj, lc[(j & 1) * 32 + k], r[k]);
+        }
+      }
+      __syncwarp();
+#ifdef CSB_LEAF_PROFILE
+      if (lane == 0) g_leaf_clk[20 + kb] = clock64();
+#endif
+      double dl = r[0];
+#pragma unroll
+      for (int k = 1; k < 32; ++k)
+        if (k == lane) dl = r[k];
+      const double my_inv = 1.0 / dl;  // 1 / L(lane, lane): one division per lane, in parallel
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (k <= lane) at(c0 + lane, c0 + k) = r[k];
+      __syncwarp();
+#ifdef CSB_LEAF_PROFILE
+      if (lane == 0) g_leaf_clk[24 + kb] = clock64();
+#endif
+      // X_kk = L_kk^-1 column-parallel: lane j owns column j;
+      // X(i, j) = -(sum_{k=j}^{i-1} L(i, k) X(k, j)) / L(i, i)
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const double ii = __shfl_sync(0xffffffffu, my_inv, i);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = fma(at(c0 + i, c0 + k), x[k], s);
+        x[i] = i < lane ? 0.0 : (i == lane ? ii : -s * ii);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i >= lane) at(c0 + i, c0 + lane) = x[i];  // the block's upper part stays 0
     }
     __syncthreads();
-    const double piv = S[k * kLeafLd + k];
-    for (int i = k + 1 + tid; i < b; i += kLeafThreads) S[k * kLeafLd + i] /= piv;
-    __syncthreads();
-    if (jc > k && jc < b) {
-      const double ljk = S[k * kLeafLd + jc];
-      for (int i = jc + q; i < b; i += kLeafThreads / kLeaf) S[jc * kLeafLd + i] -= S[k * kLeafLd + i] * ljk;
+    LEAF_MARK(2 + 3 * kb);
+    const int rem = nb - kb - 1;  // 32-blocks below / right of this one
+    if (rem == 0) break;
+    // panel: L_Ik = A_Ik X_kk^T for I > kb; a task owns 16 full rows (both
+    // column quadrants), so it reads its rows completely before writing them
+    for (int task = warp; task < rem * 2; task += kWarps) {
+      const int I = kb + 1 + (task >> 1), qi = (task & 1) * 16;
+      double acc[2][2][2][2] = {};
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        dmma::warp_mma16(
+            acc[h], 32, [&](int i, int k) { return at(32 * I + qi + i, c0 + k); },
+            [&](int k, int j) { return at(c0 + 16 * h + j, c0 + k); }, g, tq);  // X_kk(j, k): 0 for k > j
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              at(32 * I + qi + 8 * a + g, c0 + 16 * h + 8 * bb + 2 * tq + c) = acc[h][a][bb][c];
     }
     __syncthreads();
-  }
-  // in-place inverse, columns right to left; 4 threads per row share the sum
-  const int row = tid / 4, part = tid % 4;
-  for (int j = b - 1; j >= 0; --j) {
-    if (tid < b) col[tid] = S[j * kLeafLd + tid];  // L(:, j) (rows > j) before it is overwritten
-    __syncthreads();
-    const double ljj = col[j];
-    double s = 0.0;
-    if (row > j && row < b) {
-      for (int k = j + 1 + part; k <= row; k += 4) s += S[k * kLeafLd + row] * col[k];
+    LEAF_MARK(3 + 3 * kb);
+    // trailing: A_IJ -= L_Ik L_Jk^T for I >= J > kb (lower blocks; diagonal
+    // blocks keep their upper part untouched)
+    {
+      const int nblk = rem * (rem + 1) / 2;
+      for (int task = warp; task < nblk * 4; task += kWarps) {
+        const int q = task >> 2;
+        int bi = 0;
+        while ((bi + 1) * (bi + 2) / 2 <= q) ++bi;
+        const int bj = q - bi * (bi + 1) / 2;
+        const int I = kb + 1 + bi, J = kb + 1 + bj;
+        const int qi = ((task >> 1) & 1) * 16, qj = (task & 1) * 16;
+        if (I == J && qi < qj) continue;  // upper quadrant of a diagonal block
+        double acc[2][2][2] = {};
+        dmma::warp_mma16(
+            acc, 32, [&](int i, int k) { return at(32 * I + qi + i, c0 + k); },
+            [&](int k, int j) { return at(32 * J + qj + j, c0 + k); }, g, tq);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int i = 32 * I + qi + 8 * a + g, j = 32 * J + qj + 8 * bb + 2 * tq + c;
+              if (i >= j) at(i, j) -= acc[a][bb][c];
+            }
+      }
     }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
     __syncthreads();
-    if (part == 0 && row > j && row < b) S[j * kLeafLd + row] = -s / ljj;
-    if (tid == 0) S[j * kLeafLd + j] = 1.0 / ljj;
+    LEAF_MARK(4 + 3 * kb);
+  }
+  // inverse phase: X_IJ for I - J = d.  Storage: X_II in place of L_II
+  // (lower, upper part 0), X_IJ (I > J) column-major in Xo.  Quadrant
+  // tasks: (pair p, 16 x 16 quadrant)
+  for (int d = 1; d < nb; ++d) {
+    const int npairs = nb - d;
+    // T_p = sum_{K=J}^{I-1} L_IK X_KJ for pair p = (I = J + d, J = p)
+    for (int task = warp; task < npairs * 4; task += kWarps) {
+      const int p = task >> 2, I = p + d, J = p, qi = ((task >> 1) & 1) * 16, qj = (task & 1) * 16;
+      double acc[2][2][2] = {};
+      dmma::warp_mma16(
+          acc, 32, [&](int i, int k) { return at(32 * I + qi + i, 32 * J + k); },
+          [&](int k, int j) { return at(32 * J + k, 32 * J + qj + j); }, g, tq);  // X_JJ in place
+      for (int K = J + 1; K < I; ++K)
+        dmma::warp_mma16(
+            acc, 32, [&](int i, int k) { return at(32 * I + qi + i, 32 * K + k); },
+            [&](int k, int j) { return xo(K, J)[(qj + j) * kLeafTLd + k]; }, g, tq);  // X_KJ (K > J)
+      double* t = Tm + p * 32 * kLeafTLd;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) t[(qj + 8 * bb + 2 * tq + c) * kLeafTLd + qi + 8 * a + g] = acc[a][bb][c];
+    }
     __syncthreads();
+    // X_IJ = -X_II T_p
+    for (int task = warp; task < npairs * 4; task += kWarps) {
+      const int p = task >> 2, I = p + d, J = p, qi = ((task >> 1) & 1) * 16, qj = (task & 1) * 16;
+      const double* t = Tm + p * 32 * kLeafTLd;
+      double acc[2][2][2] = {};
+      dmma::warp_mma16(
+          acc, 32, [&](int i, int k) { return at(32 * I + qi + i, 32 * I + k); },
+          [&](int k, int j) { return t[(qj + j) * kLeafTLd + k]; }, g, tq);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            xo(I, J)[(qj + 8 * bb + 2 * tq + c) * kLeafTLd + qi + 8 * a + g] = -acc[a][bb][c];
+    }
+    __syncthreads();
+    LEAF_MARK(14 + d);
   }
-  for (int e = tid; e < b * b; e += kLeafThreads) {
-    const int i = e % b, jj = e / b;
-    X[(r0 + i) + (r0 + jj) * m] = i >= jj ? S[jj * kLeafLd + i] : 0.0;
-  }
-  if (tid == 0 && bad) atomicExch(fail, 1);
+  for (int j = warp; j < b; j += kLeafThreads / 32)
+    for (int i = lane; i < b; i += 32)
+      X[(r0 + i) + (r0 + j) * ldx] =
+          i < j ? 0.0 : ((i >> 5) == (j >> 5) ? at(i, j) : xo(i >> 5, j >> 5)[(j & 31) * kLeafTLd + (i & 31)]);
+  if (warp == 0 && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(fail, 1);
+  LEAF_MARK(18);
 }
 
 }  // namespace csb

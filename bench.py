@@ -15,7 +15,8 @@ C-ABI call `cs_mset_estimate` (pinned FP64 host observations in, FP64
 estimates + residuals out; H2D and D2H inside the timed region).  Beside the
 headline: `train` (FP64 train incl. the eigen spectrum, the reference's
 train contract), `c1` (BASELINE configs[0]), `c3` (configs[2], incl. e2e),
-`c5` (configs[4] made admissible), `sweep` (configs[3]), `sprt`,
+`c5` (configs[4] made admissible: rank 0 trains once, NCCL broadcast of
+the packed model, 10M observations sharded over the ranks), `sweep` (configs[3]), `sprt`,
 `roofline`, `cpu_baseline` (the CPU oracle on this box's host cores).
 Multi-GPU: one process per GPU, independent observation shards (weak
 scaling), no data-path collective; barrier + max-over-ranks timing.
@@ -426,7 +427,7 @@ def run_large(local, n, N, m, workload, passes=5, e2e_obs=0, cpu_obs=0):
            "outputs_checked": ok}
     fp64 = load_probe_peaks().get("dmma_f64_tflops")
     if fp64:
-        tf = _train_flops(n, m) / (statistics.median(tt) * 1e-3) / 1e12
+        tf = _train_flops(n, m) / statistics.median(tt) / 1e12  # tt in seconds
         out["train_roofline"] = {"bound": "fp64 tensor (DMMA)", "achieved": tf, "peak": fp64, "unit": "TFLOP/s",
                                  "frac": tf / fp64, "flops": _train_flops(n, m),
                                  "note": "Gram 2m^2n + Cholesky m^3/3 + inverse 4m^3/3 + P 2nm^2 over the "
@@ -455,12 +456,112 @@ def run_c3(args, local):
                      e2e_obs=250_000, cpu_obs=0 if args.no_cpu_baseline else 1500)
 
 
-def run_c5(args, local):
-    """BASELINE configs[4] made admissible (m >= 2n, so n=4,000
-    with m=8,000): one GPU's shard of 10M / 8 = 1.25M observations."""
-    return run_large(local, 4000, 1_250_000, 8000,
-                     "C5': n=4000, m=8000 (32k training rows), 1.25M observations = one of 8 shards "
-                     "of 10M, FP32 device-resident I/O", passes=3)
+C5_N, C5_n, C5_m, C5_CHUNK = 10_000_000, 4000, 8000, 1_250_000
+
+
+def run_c5(args, world, rank, local, barrier, max_over_ranks):
+    """BASELINE configs[4] made admissible (m >= 2n, so n = 4,000
+    with m = 8,000), sharded as SURVEY 8(e) specifies: rank 0 trains ONCE,
+    the packed device model is broadcast over NCCL (one buffer,
+    paper_2003_08011_b200/shard.py), and the 10M observations are split into
+    contiguous per-rank shards with no collective inside the surveillance
+    loop.  The observation stream is a fixed grid of 8 chunks of 1.25M (each
+    synthesized on the device from derive_seed(base, [1, chunk]), outside
+    the timed region), so the data -- and, by construction, every output
+    bit -- is the same at 1, 2, 4 or 8 GPUs: the line carries an exact
+    digest of all estimates (sum of their FP32 words) to show it.  Strong
+    scaling: total work fixed at 10M observations."""
+    import torch
+    import torch.distributed as dist
+    import paper_2003_08011_b200 as p
+    from paper_2003_08011_b200.shard import broadcast_model, shard_digest, shard_range, wrap64
+    dev = torch.device("cuda", local)
+    t = TEMPLATE
+    n, m = C5_n, C5_m
+    base = p.cell_data_seed(MASTER_SEED, n, C5_N, m, 0)
+    spec = lambda rows, seed: p.SignalSpec.uniform(n, rows, t["phi"], t["rho"], t["var"], t["skew"],  # noqa: E731
+                                                   t["kurt"], seed)
+    backend = p.BackendId("b200", local, "fp32")
+    out = {"workload": "C5': n=4000, m=8000 (32k training rows), N=10M observations sharded over the ranks, "
+                       "FP32 device-resident I/O",
+           "n_signals": n, "n_memory": m, "n_observations": C5_N, "n_gpus": world, "scaling": "strong",
+           "chunks": C5_N // C5_CHUNK}
+    model = None
+    if rank == 0:
+        X = p.synthesize_device(spec(TRAIN_FACTOR * m, p.derive_seed(base, [0])), local)
+        os.environ["CSB_EAGER_SPECTRUM"] = "1"
+        tt_eager, _ = _train_times(p, lambda: p.train_device(X, m, p.KernelConfig(), backend), 2)
+        del os.environ["CSB_EAGER_SPECTRUM"]
+        tt, model = _train_times(p, lambda: p.train_device(X, m, p.KernelConfig(), backend), 3)
+        del X
+        torch.cuda.empty_cache()
+        out.update(train_ms=statistics.median(tt_eager) * 1e3, train_ms_min=min(tt_eager) * 1e3,
+                   train_ms_spectrum_deferred=statistics.median(tt) * 1e3,
+                   train_api="cs_mset_train_device on rank 0 only (device FP64 training rows, synchronous); "
+                             "train_ms includes the eigen spectrum (mset.cpp:153-154)")
+        fp64 = load_probe_peaks().get("dmma_f64_tflops")
+        if fp64:
+            tf = _train_flops(n, m) / statistics.median(tt) / 1e12
+            out["train_roofline"] = {"bound": "fp64 tensor (DMMA)", "achieved": tf, "peak": fp64,
+                                     "unit": "TFLOP/s", "frac": tf / fp64, "flops": _train_flops(n, m),
+                                     "note": "Gram 2m^2n + Cholesky m^3/3 + inverse 4m^3/3 + P 2nm^2 over the "
+                                             "spectrum-deferred train time"}
+    # ---- broadcast of the trained model (one packed device buffer)
+    barrier()
+    t0 = time.perf_counter()
+    if world > 1:
+        model, wire_bytes = broadcast_model(model, backend, src=0)
+    else:
+        wire_bytes = p.pack_model(model).numel()
+    barrier()
+    bcast_s = time.perf_counter() - t0
+    # ---- this rank's chunks of the fixed 8-chunk observation grid
+    c0, c1 = shard_range(C5_N // C5_CHUNK, world, rank, align=1)
+    ms_total, digest = 0.0, 0
+    st = torch.cuda.current_stream(dev)
+    obs = est = res = None
+    for c in range(c0, c1):
+        obs = None
+        torch.cuda.empty_cache()
+        obs = p.synthesize_device(spec(C5_CHUNK, p.derive_seed(base, [1, c])), local, dtype=torch.float32)
+        torch.cuda.empty_cache()
+        if est is None:
+            est, res = torch.empty_like(obs.T).T, torch.empty_like(obs.T).T
+            p.estimate_device(model, obs, est, res, st)  # warm-up (lazy operand setup)
+        ms = _device_pass_timer(p, torch, model, obs, est, res, st, 1)[0]
+        ms_total += ms
+        digest = wrap64(digest + shard_digest(est))
+        if c == c0 and not bool(torch.allclose(res, obs - est)):
+            raise RuntimeError("C5': residual identity failed")
+    del obs, est, res
+    torch.cuda.empty_cache()
+    ms_max = max_over_ranks(ms_total)
+    d = torch.tensor([digest], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(d)
+    if rank != 0:
+        del model
+        return None
+    flops = 4.0 * n * m * C5_N
+    p_eff = load_peaks().get("bf16_tflops", 1590.0) / 3
+    out.update(obs_per_s=C5_N / (ms_max * 1e-3), ms_estimate_max_over_ranks=ms_max,
+               broadcast_ms=bcast_s * 1e3, model_wire_bytes=wire_bytes,
+               collective="NCCL broadcast of the packed model (torch.distributed, %d ranks)" % world
+               if world > 1 else "none (1 rank)",
+               obs_per_s_incl_train_and_broadcast=C5_N / (out["train_ms_spectrum_deferred"] * 1e-3 + bcast_s
+                                                          + ms_max * 1e-3),
+               estimates_digest=wrap64(int(d.item())),
+               digest_note="sum of the FP32 words of all 10M x 4000 estimates (int64, wrapping): equal at "
+                           "every GPU count when the sharded outputs are bitwise equal",
+               algorithmic_tflops=flops / (ms_max * 1e-3) / 1e12,
+               roofline={"bound": "tensor", "peak": p_eff, "unit": "TFLOP/s",
+                         "frac": flops / (ms_max * 1e-3) / 1e12 / (p_eff * world),
+                         "peak_note": "measured dense bf16 (MEASURED_PEAKS.json) / 3 per GPU x n_gpus"},
+               kernels="pack_obs + obs_sqnorm + gemm3x_f16_kernel<256,EpiSim> + gemm3x_f16_kernel<256,EpiOut> "
+                       "per observation block")
+    del model
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_c1(args, local, reps):
@@ -514,10 +615,13 @@ def run_c1(args, local, reps):
     return out
 
 
-def run_sprt_bench(local, n=100, N=1_000_000, reps=5):
-    """SPRT over device-resident FP32 residuals (N x n column-major): the
-    synchronous cs_sprt_device call (speculate + fix-up + count kernels),
-    residual bytes read + flag bytes written per second against the HBM peak."""
+def run_sprt_bench(local, n=1000, N=1_000_000, reps=5):
+    """SPRT over device-resident FP32 residuals (N x n column-major; the C3
+    surveillance output shape): cs_sprt_device = speculate pass (staged,
+    coalesced, vectorised residual reads and flag stores) + fix-up pass (warp
+    per signal) + the small state / count copies, CUDA events on the stream
+    it runs on.  Bytes: FP32 residual in (4 B) + flag byte out (1 B) per
+    (observation, signal), against the HBM peak."""
     import numpy as np
     import torch
     import paper_2003_08011_b200 as p
@@ -525,21 +629,29 @@ def run_sprt_bench(local, n=100, N=1_000_000, reps=5):
     g = torch.Generator(device=dev).manual_seed(7)
     resid = torch.randn((n, N), generator=g, device=dev, dtype=torch.float32).T
     det = p.SprtDetector(np.ones(n), backend=p.BackendId("b200", local, "fp32"))
-    det.update_device(resid)
+    st = torch.cuda.current_stream(dev)
+    det.update_device(resid, stream=st)
     torch.cuda.synchronize()
-    ts = []
+    ms, walls = [], []
     for _ in range(reps):
         det.state[:] = 0.0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, counts = det.update_device(resid)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
+        a.record(st)
+        _, counts = det.update_device(resid, stream=st)
+        b.record(st)
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t0)
+        ms.append(a.elapsed_time(b))
+    t = statistics.median(ms) * 1e-3
     gbs = (4.0 + 1.0) * n * N / t / 1e9
     hbm = load_peaks().get("hbm_gbs", 6650.0)
-    return {"n_signals": n, "n_observations": N, "ms": t * 1e3, "flags_per_s": n * N / t,
-            "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm, "alarms": int(counts.sum()),
-            "note": "wall time of the synchronous cs_sprt_device call incl. its host state/count copies; "
+    return {"n_signals": n, "n_observations": N, "ms": t * 1e3, "wall_ms": statistics.median(walls) * 1e3,
+            "flags_per_s": n * N / t, "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
+            "alarms": int(counts.sum()),
+            "kernels": "sprt_speculate_kernel<float,true> + sprt_fixup_kernel<float>",
+            "note": "CUDA events around the cs_sprt_device call on its stream (kernels + state/count copies); "
                     "FP32 residuals in (4 B), byte flags out (1 B) per (observation, signal)"}
 
 
@@ -616,6 +728,9 @@ def run_b200(args, world, rank, local):
     clocks = sampler.stop()
     e2e_mean = max_over_ranks(statistics.mean(e2e_t))
 
+    # ---- C5' (configs[4]): train once, broadcast, observation shards
+    c5 = None if args.no_c5 else run_c5(args, world, rank, local, barrier, max_over_ranks)
+
     # ---- Monte Carlo scoping sweep (cells/s), strong scaling over ranks
     sweep = None if args.no_sweep else run_bench_sweep(world, rank, local, barrier, max_over_ranks)
 
@@ -664,13 +779,13 @@ def run_b200(args, world, rank, local):
     }
     if sweep is not None:
         line["sweep"] = sweep
+    if c5 is not None:
+        line["c5"] = c5
     if world == 1:
         if not args.no_c1:
             line["c1"] = run_c1(args, local, args.steps)
         if not args.no_c3:
             line["c3"] = run_c3(args, local)
-        if not args.no_c5:
-            line["c5"] = run_c5(args, local)
         if not args.no_sprt:
             line["sprt"] = run_sprt_bench(local)
         if not args.no_cpu_baseline:

@@ -153,6 +153,22 @@ cs_status cs_model_import(cs_ctx* ctx, int64_t n, int64_t m, int kernel_kind,
                           cs_model** out);
 cs_status cs_model_destroy(cs_model* model);
 
+/* Model wire format (multi-GPU C5'): the whole device model --
+ * header, source indices, spectrum, D, D_norm, scale, G+, and the packed
+ * FP32 tensor-core operand tiles -- as ONE contiguous device buffer, so a
+ * trained model moves between GPUs with a single collective (NCCL
+ * broadcast over NVLink) and no host round trip.  No reference counterpart:
+ * the reference trains and estimates in one process on one host
+ * (mset.cpp:139-199); this is the broadcast step of "train once, shard the
+ * observations".  Unpacking copies into a new model on ctx's device whose
+ * estimates are bitwise those of the packed model.  Errors: CS_CONFIG_ERROR
+ * for a short buffer, CS_IO_ERROR for a buffer that is not a model wire. */
+cs_status cs_model_wire_size(const cs_model* model, int64_t* bytes);
+cs_status cs_model_pack_device(cs_ctx* ctx, const cs_model* model,
+                               void* d_wire, int64_t bytes);
+cs_status cs_model_unpack_device(cs_ctx* ctx, const void* d_wire,
+                                 int64_t bytes, cs_model** out);
+
 /* CSM1 model files (save_model / load_model, mset.cpp:225-310; declared at
  * mset.hpp:83-86): byte-compatible with the reference writer, including the
  * "<path>.json" sidecar.  Errors: CS_IO_ERROR with the reference texts

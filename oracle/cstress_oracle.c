@@ -407,14 +407,21 @@ int or_synthesize(int64_t n, int64_t N, double phi, const double* corr,
       return fail(OR_BAD_CORRELATION, "synthesize: Cholesky failed");
     }
     double* row = dalloc((size_t)n);
+    /* row-major copy of the factor: the same products summed in the same
+     * order (k = 0..s), without a 8n-byte stride per term */
+    double* lrow = dalloc((size_t)n * (size_t)n);
+    for (int64_t s = 0; s < n; ++s)
+      for (int64_t k = 0; k <= s; ++k) lrow[(size_t)s * (size_t)n + (size_t)k] = CM(rep, n, s, k);
     for (int64_t t = 0; t < N; ++t) {
       for (int64_t k = 0; k < n; ++k) row[k] = z[(size_t)t + (size_t)k * (size_t)N];
       for (int64_t s = 0; s < n; ++s) {
+        const double* ls = lrow + (size_t)s * (size_t)n;
         double acc = 0.0;
-        for (int64_t k = 0; k <= s; ++k) acc += row[k] * CM(rep, n, s, k);
+        for (int64_t k = 0; k <= s; ++k) acc += row[k] * ls[k];
         z[(size_t)t + (size_t)s * (size_t)N] = acc;
       }
     }
+    free(lrow);
     free(row);
     free(rep);
   }

@@ -47,6 +47,9 @@ _SIGNATURES = {
     "cs_model_export": (i32, [vp, pi64, pd, pd, pd, pd]),
     "cs_model_import": (i32, [vp, i64, i64, i32, d, i64, pi64, pd, pd, pd, pd, i32, P(vp)]),
     "cs_model_destroy": (i32, [vp]),
+    "cs_model_wire_size": (i32, [vp, pi64]),
+    "cs_model_pack_device": (i32, [vp, vp, vp, i64]),
+    "cs_model_unpack_device": (i32, [vp, vp, i64, P(vp)]),
     "cs_model_save": (i32, [vp, C.c_char_p]),
     "cs_sprt": (i32, [vp, pd, i64, i64, pd, pd, d, d, pd, P(C.c_uint8), pi64]),
     "cs_sprt_device": (i32, [vp, vp, i32, i64, i64, i64, pd, pd, d, d, pd, vp, pi64]),

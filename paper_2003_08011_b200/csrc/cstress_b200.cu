@@ -1107,19 +1107,26 @@ void sprt_device(cs_ctx* ctx, const IO* resid, int64_t N, int64_t n, int64_t ld,
       fail(CS_CONFIG_ERROR, "sprt: per-signal coefficients must be finite and c > 0");
   if (!(A < 0.0 && B > 0.0)) fail(CS_CONFIG_ERROR, "sprt: thresholds must satisfy A < 0 < B");
   if (N == 0 || n == 0) return;
+  if (n > 65535) fail(CS_CONFIG_ERROR, "sprt: at most 65535 signals per call");
   const int chunks = static_cast<int>((N + kSprtChunk - 1) / kSprtChunk);
-  TmpBuf<double> dc(n), dh(n), dstate(2 * n), spec(static_cast<size_t>(2) * n * chunks);
+  TmpBuf<double> dc(n), dh(n), dstate(2 * n);
+  TmpBuf<SprtChunk> rec(static_cast<size_t>(n) * chunks);
   TmpBuf<unsigned long long> dcount(2 * n);
   CSB_CUDA(cudaMemcpyAsync(dc.get(), c, n * 8, cudaMemcpyHostToDevice, st));
   CSB_CUDA(cudaMemcpyAsync(dh.get(), h, n * 8, cudaMemcpyHostToDevice, st));
   CSB_CUDA(cudaMemcpyAsync(dstate.get(), state, 2 * n * 8, cudaMemcpyHostToDevice, st));
-  sprt_speculate_kernel<IO><<<grid_for(n * chunks, 128), 128, 0, st>>>(
-      resid, N, static_cast<int>(n), ld, dc.get(), dh.get(), A, B, dstate.get(), chunks, d_flags, spec.get());
+  const bool vec = (reinterpret_cast<uintptr_t>(resid) % 16 == 0) && ((ld * sizeof(IO)) % 16 == 0);
+  const dim3 grid(ceil_div(chunks, kSprtCta), static_cast<unsigned>(n));
+  if (vec)
+    sprt_speculate_kernel<IO, true><<<grid, kSprtCta, 0, st>>>(resid, N, ld, dc.get(), dh.get(), A, B,
+                                                               dstate.get(), chunks, d_flags, rec.get());
+  else
+    sprt_speculate_kernel<IO, false><<<grid, kSprtCta, 0, st>>>(resid, N, ld, dc.get(), dh.get(), A, B,
+                                                                dstate.get(), chunks, d_flags, rec.get());
   CSB_LAUNCH_CHECK();
-  sprt_fixup_kernel<IO><<<ceil_div(n, 64), 64, 0, st>>>(resid, N, static_cast<int>(n), ld, dc.get(), dh.get(), A,
-                                                        B, dstate.get(), chunks, d_flags, spec.get());
-  CSB_LAUNCH_CHECK();
-  sprt_count_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(d_flags, N, static_cast<int>(n), dcount.get());
+  sprt_fixup_kernel<IO><<<ceil_div(n, 4), 128, 0, st>>>(resid, N, static_cast<int>(n), ld, dc.get(), dh.get(),
+                                                         A, B, dstate.get(), chunks, d_flags, rec.get(),
+                                                         dcount.get());
   CSB_LAUNCH_CHECK();
   std::vector<unsigned long long> hc(2 * n);
   CSB_CUDA(cudaMemcpyAsync(state, dstate.get(), 2 * n * 8, cudaMemcpyDeviceToHost, st));
@@ -1601,6 +1608,153 @@ cs_status cs_model_destroy(cs_model* M) {
     cudaSetDevice(M->device);
     cudaDeviceSynchronize();  // no call may still read the model's buffers
     delete M;
+  });
+}
+
+}  // extern "C"
+
+// ================================================================ model wire
+// One contiguous device buffer per model (include/cstress_b200.h, "Model
+// wire format"): [header 1 KiB][source indices m x i64][spectrum m x f64]
+// [device buffers, each 256-byte aligned, in visit order].  The receiving
+// rank reads only the header back to the host; the payload stays on the
+// device (D2D copies), so a broadcast of the buffer is the whole transfer.
+namespace {
+
+constexpr char kWireMagic[8] = {'C', 'S', 'B', 'W', 'I', 'R', 'E', '1'};
+constexpr int kWireBuffers = 16;
+constexpr int64_t kWireHeader = 1024;
+
+struct WireHeader {
+  char magic[8];
+  int64_t total_bytes;
+  int64_t n, m, rank;
+  int32_t kind, precision;
+  double h;
+  int32_t spectrum_ready, tc, MT, NB, SB, K1, N2, m_tiles, n_stages, gemm;
+  int32_t bnA, ntA, kcA, bnB, ntB, kcB;
+  float dd_max, aug_x;
+  int64_t count[kWireBuffers];  // elements per device buffer
+  int64_t elem[kWireBuffers];   // element size per device buffer
+};
+static_assert(sizeof(WireHeader) <= kWireHeader, "wire header exceeds its slot");
+
+// every device buffer of a model, in wire order (the one place that lists them)
+template <class M, class F>
+void visit_model_buffers(M* model, F&& f) {
+  f(model->D); f(model->Dn); f(model->scale); f(model->pinv); f(model->spectrum);
+  f(model->dn_tiles); f(model->p_tiles); f(model->dd); f(model->dn32); f(model->inv_scale);
+  f(model->scale_f); f(model->scale_out_f); f(model->p_shift); f(model->scale_out_d);
+  f(model->dn_gemm); f(model->p_gemm);
+}
+
+int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+WireHeader wire_header(const cs_model* M) {
+  WireHeader w;
+  std::memset(&w, 0, sizeof w);
+  std::memcpy(w.magic, kWireMagic, 8);
+  w.n = M->n; w.m = M->m; w.rank = M->rank; w.kind = M->kind; w.precision = M->precision; w.h = M->h;
+  w.spectrum_ready = M->spectrum_ready ? 1 : 0;
+  w.tc = M->tc; w.MT = M->MT; w.NB = M->NB; w.SB = M->SB; w.K1 = M->K1; w.N2 = M->N2;
+  w.m_tiles = M->m_tiles; w.n_stages = M->n_stages; w.gemm = M->gemm;
+  w.bnA = M->bnA; w.ntA = M->ntA; w.kcA = M->kcA; w.bnB = M->bnB; w.ntB = M->ntB; w.kcB = M->kcB;
+  w.dd_max = M->dd_max; w.aug_x = M->aug_x;
+  int i = 0;
+  visit_model_buffers(M, [&](const auto& b) {
+    w.count[i] = static_cast<int64_t>(b.count);
+    w.elem[i] = static_cast<int64_t>(sizeof(*b.ptr));
+    ++i;
+  });
+  int64_t off = kWireHeader + align256(16 * w.m);
+  for (int k = 0; k < kWireBuffers; ++k) off += align256(w.count[k] * w.elem[k]);
+  w.total_bytes = off;
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+cs_status cs_model_wire_size(const cs_model* M, int64_t* bytes) {
+  return guarded([&] {
+    if (!M || !bytes) fail(CS_CONFIG_ERROR, "cs_model_wire_size: null argument");
+    *bytes = wire_header(M).total_bytes;
+  });
+}
+
+cs_status cs_model_pack_device(cs_ctx* ctx, const cs_model* M, void* d_wire, int64_t bytes) {
+  return guarded([&] {
+    if (!ctx || !M || !d_wire) fail(CS_CONFIG_ERROR, "cs_model_pack_device: null argument");
+    if (M->device != ctx->device) fail(CS_CONFIG_ERROR, "cs_model_pack_device: model lives on another device");
+    set_device(ctx->device);
+    std::lock_guard<std::mutex> lock(M->spectrum_mu);  // not mid-materialisation
+    const WireHeader w = wire_header(M);
+    if (bytes < w.total_bytes) fail(CS_CONFIG_ERROR, "cs_model_pack_device: wire buffer too small");
+    cudaStream_t st = ctx->stream;
+    auto* base = static_cast<unsigned char*>(d_wire);
+    const int64_t m = M->m;
+    std::vector<unsigned char> host(kWireHeader + 16 * m, 0);
+    std::memcpy(host.data(), &w, sizeof w);
+    std::memcpy(host.data() + kWireHeader, M->source_indices.data(), 8 * m);
+    std::memcpy(host.data() + kWireHeader + 8 * m, M->spectrum_host.data(), 8 * m);
+    CSB_CUDA(cudaMemcpyAsync(base, host.data(), host.size(), cudaMemcpyHostToDevice, st));
+    int64_t off = kWireHeader + align256(16 * m);
+    visit_model_buffers(M, [&](const auto& b) {
+      const int64_t nb = static_cast<int64_t>(b.count * sizeof(*b.ptr));
+      if (nb) CSB_CUDA(cudaMemcpyAsync(base + off, b.ptr, nb, cudaMemcpyDeviceToDevice, st));
+      off += align256(nb);
+    });
+    CSB_CUDA(cudaStreamSynchronize(st));  // `host` is pageable: complete before it goes
+  });
+}
+
+cs_status cs_model_unpack_device(cs_ctx* ctx, const void* d_wire, int64_t bytes, cs_model** out) {
+  return guarded([&] {
+    if (!ctx || !d_wire || !out) fail(CS_CONFIG_ERROR, "cs_model_unpack_device: null argument");
+    if (bytes < kWireHeader) fail(CS_CONFIG_ERROR, "cs_model_unpack_device: buffer shorter than the header");
+    set_device(ctx->device);
+    cudaStream_t st = ctx->stream;
+    StreamScope scope(st);
+    const auto* base = static_cast<const unsigned char*>(d_wire);
+    WireHeader w;
+    CSB_CUDA(cudaMemcpyAsync(&w, base, sizeof w, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    if (std::memcmp(w.magic, kWireMagic, 8) != 0)
+      fail(CS_IO_ERROR, "cs_model_unpack_device: not a model wire buffer (bad magic)");
+    if (w.total_bytes > bytes)
+      fail(CS_CONFIG_ERROR, "cs_model_unpack_device: buffer shorter than the wire it holds");
+    if (w.n < 1 || w.m < 1) fail(CS_IO_ERROR, "cs_model_unpack_device: corrupt header");
+    check_kind(w.kind);
+    std::unique_ptr<cs_model> M(new cs_model);
+    M->device = ctx->device;
+    M->n = w.n; M->m = w.m; M->rank = w.rank; M->kind = w.kind; M->precision = w.precision; M->h = w.h;
+    M->spectrum_ready = w.spectrum_ready != 0;
+    M->tc = w.tc; M->MT = w.MT; M->NB = w.NB; M->SB = w.SB; M->K1 = w.K1; M->N2 = w.N2;
+    M->m_tiles = w.m_tiles; M->n_stages = w.n_stages; M->gemm = w.gemm;
+    M->bnA = w.bnA; M->ntA = w.ntA; M->kcA = w.kcA; M->bnB = w.bnB; M->ntB = w.ntB; M->kcB = w.kcB;
+    M->dd_max = w.dd_max; M->aug_x = w.aug_x;
+    const int64_t m = w.m;
+    M->source_indices.resize(m);
+    M->spectrum_host.resize(m);
+    CSB_CUDA(cudaMemcpyAsync(M->source_indices.data(), base + kWireHeader, 8 * m, cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), base + kWireHeader + 8 * m, 8 * m,
+                             cudaMemcpyDeviceToHost, st));
+    int64_t off = kWireHeader + align256(16 * m);
+    int i = 0;
+    visit_model_buffers(M.get(), [&](auto& b) {
+      if (w.elem[i] != static_cast<int64_t>(sizeof(*b.ptr)))
+        fail(CS_IO_ERROR, "cs_model_unpack_device: wire layout from another library version");
+      const int64_t nb = w.count[i] * w.elem[i];
+      if (w.count[i]) {
+        b.resize(static_cast<size_t>(w.count[i]));
+        CSB_CUDA(cudaMemcpyAsync(b.ptr, base + off, nb, cudaMemcpyDeviceToDevice, st));
+      }
+      off += align256(nb);
+      ++i;
+    });
+    CSB_CUDA(cudaStreamSynchronize(st));
+    *out = M.release();
   });
 }
 

@@ -481,3 +481,45 @@ def estimate_device(model: TrainedModel, obs, est=None, resid=None, stream=None,
             C.c_void_p(resid.data_ptr() if resid is not None else 0)))
     finally:
         ctx.set_stream(None)
+
+
+# ------------------------------------------------------------- model wire
+def pack_model(model: TrainedModel, out=None):
+    """The whole device model as one uint8 CUDA tensor on the model's device
+    (cs_model_pack_device): what rank 0 broadcasts in the observation-sharded
+    C5' path.  `out` may be a preallocated uint8 tensor."""
+    import torch
+    nbytes = C.c_int64()
+    check(_lib.lib().cs_model_wire_size(model.handle, C.byref(nbytes)))
+    dev = torch.device("cuda", model.backend.device)
+    if out is None:
+        out = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    if out.dtype != torch.uint8 or not out.is_contiguous() or out.numel() < nbytes.value:
+        raise ShapeError("pack_model: out must be a contiguous uint8 tensor of at least the wire size")
+    _check_device(out, model.backend, "pack_model: out")
+    ctx = _ctx(model.backend)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    try:
+        check(_lib.lib().cs_model_pack_device(ctx.handle, model.handle, C.c_void_p(out.data_ptr()),
+                                              out.numel()))
+    finally:
+        ctx.set_stream(None)
+    return out
+
+
+def unpack_model(wire, backend: BackendId = BackendId()) -> TrainedModel:
+    """A model from a wire tensor (cs_model_unpack_device) on the backend's
+    device; its estimates are bitwise those of the packed model."""
+    import torch
+    if wire.dtype != torch.uint8 or not wire.is_contiguous():
+        raise ShapeError("unpack_model: wire must be a contiguous uint8 tensor")
+    _check_device(wire, backend, "unpack_model: wire")
+    ctx = _ctx(backend)
+    ctx.set_stream(torch.cuda.current_stream(wire.device).cuda_stream)
+    h = C.c_void_p()
+    try:
+        check(_lib.lib().cs_model_unpack_device(ctx.handle, C.c_void_p(wire.data_ptr()), wire.numel(),
+                                                C.byref(h)))
+    finally:
+        ctx.set_stream(None)
+    return TrainedModel(h, backend)

@@ -125,21 +125,36 @@ static double* dalloc(size_t count) {
 /* Eigen LLT unblocked semantics (Cholesky.h llt_inplace): lower L with
  * A = L L^T; fails when a pivot x <= 0.  Column-major, in place on `L`. */
 static int llt_lower(double* L, int64_t n) {
-  for (int64_t k = 0; k < n; ++k) {
-    double x = CM(L, n, k, k);
-    for (int64_t j = 0; j < k; ++j) x -= CM(L, n, k, j) * CM(L, n, k, j);
-    if (!(x > 0.0)) return 0;
+  /* Eigen::LLT order (the sums run j = 0..k-1), computed on a row-major copy
+   * so that the inner sums walk contiguous memory: identical arithmetic,
+   * without an 8n-byte stride per term (n = 4000 took an hour) */
+  double* R = dalloc((size_t)n * (size_t)n);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = j; i < n; ++i) R[(size_t)i * (size_t)n + (size_t)j] = CM(L, n, i, j);
+  int ok = 1;
+  for (int64_t k = 0; k < n && ok; ++k) {
+    double* rk = R + (size_t)k * (size_t)n;
+    double x = rk[k];
+    for (int64_t j = 0; j < k; ++j) x -= rk[j] * rk[j];
+    if (!(x > 0.0)) {
+      ok = 0;
+      break;
+    }
     x = sqrt(x);
-    CM(L, n, k, k) = x;
+    rk[k] = x;
     for (int64_t i = k + 1; i < n; ++i) {
-      double v = CM(L, n, i, k);
-      for (int64_t j = 0; j < k; ++j) v -= CM(L, n, i, j) * CM(L, n, k, j);
-      CM(L, n, i, k) = v / x;
+      double* ri = R + (size_t)i * (size_t)n;
+      double v = ri[k];
+      for (int64_t j = 0; j < k; ++j) v -= ri[j] * rk[j];
+      ri[k] = v / x;
     }
   }
-  for (int64_t j = 0; j < n; ++j)
-    for (int64_t i = 0; i < j; ++i) CM(L, n, i, j) = 0.0;
-  return 1;
+  if (ok) {
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < n; ++i) CM(L, n, i, j) = i >= j ? R[(size_t)i * (size_t)n + (size_t)j] : 0.0;
+  }
+  free(R);
+  return ok;
 }
 
 static double frob_norm(const double* A, int64_t n) {

@@ -50,13 +50,24 @@ struct SprtStep {
   double c, h, A, B;
   // one step of both tests; returns the flag bits
   __device__ __forceinline__ uint32_t operator()(double r, double& lp, double& ln) const {
-    // branch-free: decisions as predicates, resets as selects
     lp = __dadd_rn(lp, __dmul_rn(c, __dsub_rn(r, h)));
     ln = __dadd_rn(ln, __dmul_rn(c, __dsub_rn(-r, h)));
-    const bool ap = lp >= B, an = ln >= B;
-    lp = (ap || lp <= A) ? 0.0 : lp;
-    ln = (an || ln <= A) ? 0.0 : ln;
-    return static_cast<uint32_t>(ap) | (static_cast<uint32_t>(an) << 1);
+    return decide(lp) | (decide(ln) << 1);
+  }
+  // lambda >= B: alarm and reset; lambda <= A: reset -- branch-free, the
+  // reset predicate folded into the second compare (setp .or), so a
+  // decision is two compares and one 64-bit select (NaN never decides,
+  // exactly like the oracle's comparisons)
+  __device__ __forceinline__ uint32_t decide(double& l) const {
+    uint32_t f;
+    asm("{\n\t.reg .pred pa, pz;\n\t"
+        "setp.ge.f64 pa, %0, %2;\n\t"
+        "setp.le.or.f64 pz, %0, %3, pa;\n\t"
+        "selp.f64 %0, 0d0000000000000000, %0, pz;\n\t"
+        "selp.u32 %1, 1, 0, pa;\n\t}"
+        : "+d"(l), "=r"(f)
+        : "d"(B), "d"(A));
+    return f;
   }
 };
 
@@ -115,7 +126,11 @@ __global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? 6 : 4) sprt_specul
     uint8_t* __restrict__ flags, SprtChunk* __restrict__ rec) {
   using V = typename SprtVec<IO>::T;
   constexpr int kV = SprtVec<IO>::k;
-  __shared__ IO rs[kSprtCta][kSprtSeg + 1];
+  // rows padded to a 16-byte multiple (36 floats / 34 doubles): the staging
+  // writes and the per-thread row reads are both 128-bit and conflict-free
+  // (per 8-lane phase the rows start 4 banks apart)
+  constexpr int kRow = kSprtSeg + 16 / static_cast<int>(sizeof(IO));
+  __shared__ __align__(16) IO rs[kSprtCta][kRow];
   __shared__ uint32_t fw[kSprtCta][kSprtSeg / 4 + 1];
   __shared__ double sfin[kSprtCta][2];
   const int s = blockIdx.y;
@@ -128,6 +143,14 @@ __global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? 6 : 4) sprt_specul
   uint8_t* f = flags + static_cast<int64_t>(s) * N;
   double lp = k == 0 ? state[2 * s] : 0.0, ln = k == 0 ? state[2 * s + 1] : 0.0;
   uint32_t cp = 0, cn = 0;
+  // this CTA's region of the column: <= kSprtCta * kSprtChunk steps, so all
+  // offsets below are 32-bit
+  const int64_t cta_start = static_cast<int64_t>(chunk0) * kSprtChunk;
+  const IO* rc = r + cta_start;
+  uint8_t* fc = f + cta_start;
+  const int rem = static_cast<int>(min(N - cta_start, static_cast<int64_t>(kSprtCta) * kSprtChunk));
+  const int my0 = tid * kSprtChunk;
+  const int my_end = min(rem, my0 + kSprtChunk);
 
   // Staged tile of a round: kSprtCta segments (one per chunk) of kSprtSeg
   // consecutive steps.  VEC: thread `tid` loads vector tid % kLanesPerSeg of
@@ -139,75 +162,80 @@ __global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? 6 : 4) sprt_specul
   constexpr int kVecLoads = kSprtCta / kSegsPerPass;      // passes per round (VEC)
   constexpr int kWarps = kSprtCta / 32;
   constexpr int kScalarLoads = kSprtCta / kWarps;         // segments per warp per round (scalar)
-  IO pre[VEC ? kVecLoads * kV : kScalarLoads];
+  V prev[VEC ? kVecLoads : 1];
+  IO pres[VEC ? 1 : kScalarLoads];
 
   auto load_round = [&](int round) {
-    const int64_t off = static_cast<int64_t>(round) * kSprtSeg;
+    const int off = round * kSprtSeg;
     if constexpr (VEC) {
 #pragma unroll
       for (int j = 0; j < kVecLoads; ++j) {
-        const int seg = tid / kLanesPerSeg + j * kSegsPerPass;
-        const int64_t t = static_cast<int64_t>(chunk0 + seg) * kSprtChunk + off + (tid % kLanesPerSeg) * kV;
-        if (seg < n_here && t + kV <= N) {
-          const V v = __ldg(reinterpret_cast<const V*>(r + t));
-          const IO* e = reinterpret_cast<const IO*>(&v);
-#pragma unroll
-          for (int q = 0; q < kV; ++q) pre[j * kV + q] = e[q];
+        const int o = (tid / kLanesPerSeg + j * kSegsPerPass) * kSprtChunk + off + (tid % kLanesPerSeg) * kV;
+        if (o + kV <= rem) {
+          prev[j] = __ldg(reinterpret_cast<const V*>(rc + o));
         } else {
+          IO* e = reinterpret_cast<IO*>(&prev[j]);
 #pragma unroll
-          for (int q = 0; q < kV; ++q) pre[j * kV + q] = (seg < n_here && t + q < N) ? __ldg(r + t + q) : IO(0);
+          for (int q = 0; q < kV; ++q) e[q] = o + q < rem ? __ldg(rc + o + q) : IO(0);
         }
       }
     } else {
 #pragma unroll
       for (int j = 0; j < kScalarLoads; ++j) {
-        const int seg = warp + j * kWarps;
-        const int64_t t = static_cast<int64_t>(chunk0 + seg) * kSprtChunk + off + lane;
-        pre[j] = (seg < n_here && t < N) ? __ldg(r + t) : IO(0);
+        const int o = (warp + j * kWarps) * kSprtChunk + off + lane;
+        pres[j] = o < rem ? __ldg(rc + o) : IO(0);
       }
     }
   };
   auto stage_round = [&]() {
     if constexpr (VEC) {
 #pragma unroll
-      for (int j = 0; j < kVecLoads; ++j) {
-        const int seg = tid / kLanesPerSeg + j * kSegsPerPass;
-#pragma unroll
-        for (int q = 0; q < kV; ++q) rs[seg][(tid % kLanesPerSeg) * kV + q] = pre[j * kV + q];
-      }
+      for (int j = 0; j < kVecLoads; ++j)
+        *reinterpret_cast<V*>(&rs[tid / kLanesPerSeg + j * kSegsPerPass][(tid % kLanesPerSeg) * kV]) = prev[j];
     } else {
 #pragma unroll
-      for (int j = 0; j < kScalarLoads; ++j) rs[warp + j * kWarps][lane] = pre[j];
+      for (int j = 0; j < kScalarLoads; ++j) rs[warp + j * kWarps][lane] = pres[j];
     }
   };
+  // four steps of this thread's row -> one packed flag word
+  auto four = [&](int w, int valid) -> uint32_t {
+    IO x[4];
+    if constexpr (sizeof(IO) == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(&rs[tid][4 * w]);
+      x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+    } else {
+      const double2 v0 = *reinterpret_cast<const double2*>(&rs[tid][4 * w]);
+      const double2 v1 = *reinterpret_cast<const double2*>(&rs[tid][4 * w + 2]);
+      x[0] = v0.x, x[1] = v0.y, x[2] = v1.x, x[3] = v1.y;
+    }
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < valid) word |= step(static_cast<double>(x[q]), lp, ln) << (8 * q);
+    return word;
+  };
 
-  const int64_t start = static_cast<int64_t>(k) * kSprtChunk;
-  const int64_t chunk_end = min(N, start + kSprtChunk);  // this thread's end
-  const int64_t cta_start = static_cast<int64_t>(chunk0) * kSprtChunk;
-  const int rounds =
-      static_cast<int>((min(N - cta_start, static_cast<int64_t>(kSprtChunk)) + kSprtSeg - 1) / kSprtSeg);
+  const int rounds = (min(rem, kSprtChunk) + kSprtSeg - 1) / kSprtSeg;
+  const bool words_ok = (reinterpret_cast<uintptr_t>(f) & 3) == 0;
   load_round(0);
   for (int round = 0; round < rounds; ++round) {
     stage_round();
     __syncthreads();
     if (round + 1 < rounds) load_round(round + 1);  // in flight while this round is evaluated
-    const int64_t t0 = start + static_cast<int64_t>(round) * kSprtSeg;
+    const int off = round * kSprtSeg;
     if (tid < n_here) {
-      if (t0 + kSprtSeg <= chunk_end) {  // full round: no bounds checks
+      const int t0 = my0 + off;
+      if (t0 + kSprtSeg <= my_end) {  // full round: no bounds checks
 #pragma unroll
         for (int w = 0; w < kSprtSeg / 4; ++w) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) word |= step(static_cast<double>(rs[tid][4 * w + q]), lp, ln) << (8 * q);
+          const uint32_t word = four(w, 4);
           fw[tid][w] = word;
           cp += sprt_pos_count(word);
           cn += sprt_neg_count(word);
         }
       } else {
         for (int w = 0; w < kSprtSeg / 4; ++w) {
-          uint32_t word = 0;
-          for (int q = 0; q < 4; ++q)
-            if (t0 + 4 * w + q < chunk_end) word |= step(static_cast<double>(rs[tid][4 * w + q]), lp, ln) << (8 * q);
+          const uint32_t word = four(w, max(0, min(4, my_end - (t0 + 4 * w))));
           fw[tid][w] = word;
           cp += sprt_pos_count(word);
           cn += sprt_neg_count(word);
@@ -217,23 +245,22 @@ __global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? 6 : 4) sprt_specul
     __syncthreads();
     // flags back out, lane-consecutive: a warp writes 4 segments (8 words
     // each) per instruction; byte stores where the column is not 4-aligned
-    const int64_t off = static_cast<int64_t>(round) * kSprtSeg;
-    const bool words = ((reinterpret_cast<uintptr_t>(f) & 3) == 0);
-#pragma unroll 2
-    for (int base = warp * 4; base < n_here; base += kWarps * 4) {
-      const int seg = base + (lane >> 3), w = lane & 7;
-      if (seg >= n_here) continue;
-      const int64_t t = static_cast<int64_t>(chunk0 + seg) * kSprtChunk + off + 4 * w;
-      const int64_t end = min(N, static_cast<int64_t>(chunk0 + seg + 1) * kSprtChunk);
+#pragma unroll
+    for (int it = 0; it < kSprtCta / (4 * kWarps); ++it) {
+      const int seg = (it * kWarps + warp) * 4 + (lane >> 3), w = lane & 7;
+      if (seg >= n_here) break;
+      const int o = seg * kSprtChunk + off + 4 * w;
       const uint32_t word = fw[seg][w];
-      if (words && t + 4 <= end) {
-        *reinterpret_cast<uint32_t*>(f + t) = word;
+      if (words_ok && o + 4 <= rem) {
+        *reinterpret_cast<uint32_t*>(fc + o) = word;
       } else {
         for (int q = 0; q < 4; ++q)
-          if (t + q < end) f[t + q] = static_cast<uint8_t>(word >> (8 * q));
+          if (o + q < rem) fc[o + q] = static_cast<uint8_t>(word >> (8 * q));
       }
     }
   }
+  const int64_t start = cta_start + my0;
+  const int64_t chunk_end = cta_start + my_end;
   // ---- assumed-input re-run (chunks 1.. of the CTA): the predecessor's
   // speculative final state is taken as this chunk's incoming state
   sfin[tid][0] = lp;

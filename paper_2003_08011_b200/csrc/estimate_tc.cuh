@@ -147,6 +147,9 @@ __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
 #define CSB_RCP_MUFU 4  // measured (C2, n=100/m=4000): 4 beats 2 by 3-8%, n=64 within 1.5%
 #endif
 // staged readout: 8-column O chunks read per TMEM load wait
+#ifndef CSB_MAP2
+#define CSB_MAP2 0  // 1: kernel map and S split on packed FP32 pairs (FFMA2 / FADD2)
+#endif
 #ifndef CSB_RD_BATCH
 #define CSB_RD_BATCH 2
 #endif
@@ -761,11 +764,28 @@ __global__ void __launch_bounds__(tc_threads(NB, SB), 1) mset_estimate_tc_kernel
             // scale folds into the FMA exactly.  sqrt on the MUFU pipe; of
             // every four reciprocals CSB_RCP_MUFU go to MUFU, the rest to an
             // FMA-pipe Newton iteration (default: all on MUFU).
+#if CSB_MAP2
+#pragma unroll
+            for (int e = 0; e < CH; e += 2) {
+              const float2 x2 = __ffma2_rn(make_float2(ptx::sqrt_approx(v[e]), ptx::sqrt_approx(v[e + 1])),
+                                           make_float2(inv_h_s, inv_h_s),
+                                           make_float2(1.f / kSScale, 1.f / kSScale));
+              if ((e & 3) < CSB_RCP_MUFU) {
+                v[e] = ptx::rcp_approx(x2.x);
+                v[e + 1] = ptx::rcp_approx(x2.y);
+              } else {
+                const float2 y = ptx::rcp_newton2(x2);
+                v[e] = y.x;
+                v[e + 1] = y.y;
+              }
+            }
+#else
 #pragma unroll
             for (int e = 0; e < CH; ++e) {
               const float x = fmaf(ptx::sqrt_approx(v[e]), inv_h_s, 1.f / kSScale);
               v[e] = (e & 3) < CSB_RCP_MUFU ? ptx::rcp_approx(x) : ptx::rcp_newton(x);
             }
+#endif
           }
           if (valid_cols < (c + 1) * CH) {
 #pragma unroll
@@ -779,8 +799,13 @@ __global__ void __launch_bounds__(tc_threads(NB, SB), 1) mset_estimate_tc_kernel
           for (int h8 = 0; h8 < CH / 8; ++h8) {
             uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
+            for (int e = 0; e < 4; ++e) {
+#if CSB_MAP2
+              ptx::split_f16x2_v2(v[h8 * 8 + 2 * e], v[h8 * 8 + 2 * e + 1], hi[e], lo[e]);
+#else
               ptx::split_f16x2(v[h8 * 8 + 2 * e], v[h8 * 8 + 2 * e + 1], hi[e], lo[e]);
+#endif
+            }
             ptx::tmem_st4(tmem + lane_off + s_base + (c * CH + h8 * 8) / 2, hi);
             ptx::tmem_st4(tmem + lane_off + s_base + MT / 2 + (c * CH + h8 * 8) / 2, lo);
           }

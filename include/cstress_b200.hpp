@@ -282,9 +282,47 @@ class MsetAlgorithm final : public PrognosticAlgorithm {
   }
 };
 
-inline const PrognosticAlgorithm& algorithm_by_name(const std::string& name) {
+// estimator.cpp:42-60 -- the baseline predictor (column means).  Host code,
+// as in the reference: a column mean is not worth a device round trip.
+class MeanPredictor final : public PrognosticAlgorithm {
+ public:
+  struct Model final : PrognosticModel {
+    std::vector<double> means;
+  };
+  std::string name() const override { return "mean"; }
+  std::unique_ptr<PrognosticModel> train(const SignalMatrix& training, Index, const KernelConfig&,
+                                         const BackendId&) const override {
+    auto out = std::make_unique<Model>();
+    const Index N = training.n_observations(), n = training.n_signals();
+    out->means.assign(size_t(n), 0.0);
+    for (Index s = 0; s < n; ++s) {
+      double acc = 0.0;
+      for (Index t = 0; t < N; ++t) acc += training.data(t, s);
+      out->means[size_t(s)] = acc / double(N);
+    }
+    return out;
+  }
+  EstimationResult estimate(const PrognosticModel& model, const SignalMatrix& observations,
+                            const BackendId&) const override {
+    const auto* m = dynamic_cast<const Model*>(&model);
+    if (!m) throw ConfigError("model was not trained by algorithm mean");
+    const Index N = observations.n_observations(), n = observations.n_signals();
+    if (n != Index(m->means.size())) throw ShapeError("mean predictor: signal count mismatch");
+    EstimationResult r{Matrix(N, n), Matrix(N, n)};
+    for (Index s = 0; s < n; ++s)
+      for (Index t = 0; t < N; ++t) {
+        r.estimates(t, s) = m->means[size_t(s)];
+        r.residuals(t, s) = observations.data(t, s) - m->means[size_t(s)];
+      }
+    return r;
+  }
+};
+
+inline const PrognosticAlgorithm& algorithm_by_name(const std::string& name) {  // estimator.cpp:63-69
   static const MsetAlgorithm mset;
+  static const MeanPredictor mean;
   if (name == "mset2") return mset;
+  if (name == "mean") return mean;
   throw ConfigError("unknown estimator: " + name);
 }
 

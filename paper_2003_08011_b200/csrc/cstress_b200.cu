@@ -115,6 +115,9 @@ struct cs_model {
   DevBuf<float> dd, dn32, inv_scale, scale_f, scale_out_f;
   DevBuf<double> p_shift, scale_out_d;  // per-signal 2^-k_s, scale_s * 2^(k_s - 14)
   float dd_max = 0.f;  // max ||D_norm(:, i)||^2 (near-zero guard prefilter)
+  float s_center = 0.f;         // similarity centring of the two-GEMM path (gemm_tc.cuh EpiSim)
+  DevBuf<float> add_f;          // n: scale_s * s_center * rowsum(P)_s
+  DevBuf<double> add_d;
   float aug_x = 1.f;   // x's value in the ||d||^2 column (2^k_aug)
   // large-n two-GEMM path (gemm_tc.cuh), used when the fused kernel's TMEM
   // plan does not fit (n > ~130)
@@ -209,8 +212,10 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
   col_extrema_kernel<<<static_cast<unsigned>(n), 256, 0, st>>>(X, N, imin.get(), imax.get());
   CSB_LAUNCH_CHECK();
   CSB_CUDA(cudaMemsetAsync(selected.get(), 0, N, st));
-  stage1_dedupe_kernel<<<1, 1, 0, st>>>(imin.get(), imax.get(), n, selected.get(), picked.get(),
-                                        npicked.get());
+  TmpBuf<unsigned> first(N);
+  CSB_CUDA(cudaMemsetAsync(first.get(), 0xff, N * sizeof(unsigned), st));
+  stage1_dedupe_kernel<<<1, 1024, 0, st>>>(imin.get(), imax.get(), n, selected.get(), picked.get(),
+                                           npicked.get(), first.get());
   CSB_LAUNCH_CHECK();
   // stage 2
   row_norm_key_kernel<<<ceil_div(N, 256), 256, 0, st>>>(X, N, n, selected.get(), h1.get(), r1.get());
@@ -611,6 +616,29 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
   p_row_scale_kernel<<<ceil_div(n, 32), 1024, 0, st>>>(P.get(), M->scale.get(), n, m, M->p_shift.get(),
                                                          M->scale_out_d.get(), M->scale_out_f.get());
   CSB_LAUNCH_CHECK();
+  // Similarity centring (two-GEMM path): GEMM-B accumulates P (S - s_c)
+  // and the epilogue adds s_c P 1 back.  tcgen05's FP32 accumulation
+  // truncates, and with P's cancellation (sum |P s| ~ 600 |P s| at C3) the
+  // partial sums, not the products, set the error; centring S shrinks them.
+  // s_c = the kernel at the typical squared distance of two memory vectors
+  // (2 mean ||d||^2), rounded to 8 bits so that S - s_c is exact.
+  {
+    double mean_dd = 0.0;
+    for (int i = 0; i < m; ++i) mean_dd += dd_host[i];
+    mean_dd /= static_cast<double>(m);
+    const double d2 = 2.0 * mean_dd;
+    const double sk = M->kind == CS_KERNEL_GAUSSIAN ? std::exp(-d2 / (2.0 * M->h * M->h))
+                                                    : 1.0 / (1.0 + std::sqrt(d2) / M->h);
+    M->s_center = static_cast<float>(std::round(sk * 256.0) / 256.0);
+    // the fused kernel (m <= a few thousand, K = m short) does not centre:
+    // its error is ~1e-5 without, and the extra subtraction per pair cost 3%
+    if (M->tc || std::getenv("CSB_NO_CENTER")) M->s_center = 0.f;
+    M->add_d.resize(n);
+    M->add_f.resize(n);
+    p_center_add_kernel<<<ceil_div(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+        P.get(), M->scale.get(), n, m, static_cast<double>(M->s_center), M->add_d.get(), M->add_f.get());
+    CSB_LAUNCH_CHECK();
+  }
   if (M->tc) {
     M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
     M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
@@ -679,7 +707,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   gather_memory_kernel<<<grid_for(n * m), 256, 0, st>>>(X, N, n, picked.get(), m, M->D.get());
   CSB_LAUNCH_CHECK();
   M->scale.resize(n);                                        // mset.cpp:145
-  scale_seq_kernel<<<ceil_div(n, 32), 128, 0, st>>>(X, N, n, M->scale.get());
+  scale_seq_kernel<<<ceil_div(n, 4), 128, 0, st>>>(X, N, n, M->scale.get());
   CSB_LAUNCH_CHECK();
   M->Dn.resize(n * m);                                       // mset.cpp:147-149
   div_rows_kernel<<<grid_for(n * m), 256, 0, st>>>(M->D.get(), M->scale.get(), n, m, M->Dn.get());
@@ -1057,11 +1085,12 @@ void estimate_gemm(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const IO* ob
     es.g_coef = static_cast<float>(1.4426950408889634 / (2.0 * M->h * M->h));
     es.tau = 1.0f / 128.0f;
     es.dd_max = M->dd_max;
+    es.s_center = M->s_center;
     const GemmShape ga{ctx->wsX[slot].get(), M->dn_gemm.get(), mt, M->ntA, M->kcA};
     if (M->bnA == 256) launch_gemm3x<256>(ctx, st, ga, es);
     else launch_gemm3x<128>(ctx, st, ga, es);
     EpiOut<IO> eo{obs + t0, est ? est + t0 : nullptr, resid ? resid + t0 : nullptr, M->scale_out_f.get(),
-                  M->scale_out_d.get(), nc, ld, n};
+                  M->scale_out_d.get(), nc, ld, n, M->add_f.get(), M->add_d.get()};
     const GemmShape gb{ctx->wsS[slot].get(), M->p_gemm.get(), mt, M->ntB, M->kcB};
     if (M->bnB == 256) launch_gemm3x<256>(ctx, st, gb, eo);
     else launch_gemm3x<128>(ctx, st, gb, eo);
@@ -1621,8 +1650,8 @@ cs_status cs_model_destroy(cs_model* M) {
 // device (D2D copies), so a broadcast of the buffer is the whole transfer.
 namespace {
 
-constexpr char kWireMagic[8] = {'C', 'S', 'B', 'W', 'I', 'R', 'E', '1'};
-constexpr int kWireBuffers = 16;
+constexpr char kWireMagic[8] = {'C', 'S', 'B', 'W', 'I', 'R', 'E', '2'};
+constexpr int kWireBuffers = 18;
 constexpr int64_t kWireHeader = 1024;
 
 struct WireHeader {
@@ -1633,7 +1662,7 @@ struct WireHeader {
   double h;
   int32_t spectrum_ready, tc, MT, NB, SB, K1, N2, m_tiles, n_stages, gemm;
   int32_t bnA, ntA, kcA, bnB, ntB, kcB;
-  float dd_max, aug_x;
+  float dd_max, aug_x, s_center;
   int64_t count[kWireBuffers];  // elements per device buffer
   int64_t elem[kWireBuffers];   // element size per device buffer
 };
@@ -1645,7 +1674,7 @@ void visit_model_buffers(M* model, F&& f) {
   f(model->D); f(model->Dn); f(model->scale); f(model->pinv); f(model->spectrum);
   f(model->dn_tiles); f(model->p_tiles); f(model->dd); f(model->dn32); f(model->inv_scale);
   f(model->scale_f); f(model->scale_out_f); f(model->p_shift); f(model->scale_out_d);
-  f(model->dn_gemm); f(model->p_gemm);
+  f(model->dn_gemm); f(model->p_gemm); f(model->add_f); f(model->add_d);
 }
 
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -1659,7 +1688,7 @@ WireHeader wire_header(const cs_model* M) {
   w.tc = M->tc; w.MT = M->MT; w.NB = M->NB; w.SB = M->SB; w.K1 = M->K1; w.N2 = M->N2;
   w.m_tiles = M->m_tiles; w.n_stages = M->n_stages; w.gemm = M->gemm;
   w.bnA = M->bnA; w.ntA = M->ntA; w.kcA = M->kcA; w.bnB = M->bnB; w.ntB = M->ntB; w.kcB = M->kcB;
-  w.dd_max = M->dd_max; w.aug_x = M->aug_x;
+  w.dd_max = M->dd_max; w.aug_x = M->aug_x; w.s_center = M->s_center;
   int i = 0;
   visit_model_buffers(M, [&](const auto& b) {
     w.count[i] = static_cast<int64_t>(b.count);
@@ -1733,7 +1762,7 @@ cs_status cs_model_unpack_device(cs_ctx* ctx, const void* d_wire, int64_t bytes,
     M->tc = w.tc; M->MT = w.MT; M->NB = w.NB; M->SB = w.SB; M->K1 = w.K1; M->N2 = w.N2;
     M->m_tiles = w.m_tiles; M->n_stages = w.n_stages; M->gemm = w.gemm;
     M->bnA = w.bnA; M->ntA = w.ntA; M->kcA = w.kcA; M->bnB = w.bnB; M->ntB = w.ntB; M->kcB = w.kcB;
-    M->dd_max = w.dd_max; M->aug_x = w.aug_x;
+    M->dd_max = w.dd_max; M->aug_x = w.aug_x; M->s_center = w.s_center;
     const int64_t m = w.m;
     M->source_indices.resize(m);
     M->spectrum_host.resize(m);

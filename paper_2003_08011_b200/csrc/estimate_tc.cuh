@@ -147,6 +147,9 @@ __host__ __device__ constexpr size_t tc_aux_bytes(int K1) {
 #define CSB_RCP_MUFU 4  // measured (C2, n=100/m=4000): 4 beats 2 by 3-8%, n=64 within 1.5%
 #endif
 // staged readout: 8-column O chunks read per TMEM load wait
+#ifndef CSB_G1_2X
+#define CSB_G1_2X 0  // 1: GEMM1 without the x_hi * D_lo product (D_norm at FP16 precision; A/B only)
+#endif
 #ifndef CSB_MAP2
 #define CSB_MAP2 0  // 1: kernel map and S split on packed FP32 pairs (FFMA2 / FADD2)
 #endif
@@ -387,7 +390,9 @@ __global__ void __launch_bounds__(tc_threads(NB, SB), 1) mset_estimate_tc_kernel
         uint32_t ah = tmem + colXh, al = tmem + colXl;
         for (int kk = 0; kk < K1 / 16; ++kk) {
           ptx::mma_f16_ts_elect(dS, al, bh, idesc1, kk > 0 ? 1u : 0u);
+#if !CSB_G1_2X
           ptx::mma_f16_ts_elect(dS, ah, bl, idesc1, 1u);
+#endif
           ptx::mma_f16_ts_elect(dS, ah, bh, idesc1, 1u);
           bh += k_step1;
           bl += k_step1;

@@ -66,6 +66,11 @@ struct EpiSim {
   int64_t N, ld;
   int n, m, kind;
   float inv_h, g_coef, tau, dd_max;
+  // the map emits S - s_center; EpiOut adds s_center * rowsum(P) back.
+  // tcgen05's FP32 accumulation truncates, and P's cancellation makes the
+  // partial sums, not the products, set the error: centring shrinks them
+  // (C5': 1.0e-3 -> 2.8e-4 vs the oracle; profiles/accuracy_emulation.txt)
+  float s_center;
 
   __device__ float xnorm(int64_t t, int s) const {
     if (io_f64) return static_cast<float>(static_cast<const double*>(obs)[t + s * ld] / scale_d[s]);
@@ -115,6 +120,8 @@ struct EpiSim {
         v[e] = (e & 1) ? ptx::rcp_newton(x) : ptx::rcp_approx(x);
       }
     }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] -= s_center;
     if (col0 + 16 > m) {
 #pragma unroll
       for (int e = 0; e < 16; ++e)
@@ -149,6 +156,8 @@ struct EpiOut {
   const double* scale_d;
   int64_t N, ld;
   int n;
+  const float* add_f;   // s_center * rowsum(P), scaled like the estimate
+  const double* add_d;
 
   __device__ void operator()(int mt, int r, int col0, float* v) const {
     const int64_t t = static_cast<int64_t>(mt) * kGemmBM + r;
@@ -167,11 +176,11 @@ struct EpiOut {
       if (s >= n) break;
       const int64_t idx = t + static_cast<int64_t>(s) * ld;
       if constexpr (sizeof(IO) == 8) {
-        const double ev = static_cast<double>(v[e]) * scale_d[s];
+        const double ev = fma(static_cast<double>(v[e]), scale_d[s], add_d[s]);
         if (est) est[idx] = ev;
         if (resid) resid[idx] = x[e] - ev;
       } else {
-        const float ev = v[e] * scale_f[s];
+        const float ev = fmaf(v[e], scale_f[s], add_f[s]);
         if (est) est[idx] = ev;
         if (resid) resid[idx] = x[e] - ev;
       }

@@ -213,63 +213,53 @@ __global__ void finish_estimate_kernel(const double* __restrict__ en, int64_t Nc
 }
 
 // Population std per column, sequential sums (mset.cpp:44-53, mean restated
-// as a left-to-right sum; identical to the oracle).  One warp owns 32
-// columns and sums each lane's column in order; all 4 warps stream 64 x 32
-// tiles into a double buffer with cp.async (coalesced in t), so the next
-// tile's loads overlap the serial sums over the current one.
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
+// as a left-to-right sum; identical to the oracle).  One warp per column:
+// the lanes load 32 consecutive rows per instruction (coalesced 256 bytes,
+// four blocks in flight), and every lane runs the same left-to-right sum
+// over the block, values broadcast by shuffle -- the serial DADD chain is
+// the only latency left (the previous 32-columns-per-warp layout ran on
+// n / 32 SMs behind a CTA barrier per 64 rows).
 __global__ void __launch_bounds__(128)
 scale_seq_kernel(const double* __restrict__ X, int64_t N, int64_t n, double* __restrict__ scale) {
-  constexpr int R = 64;
-  __shared__ double tile[2][R][33];
-  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * 32;
-  const int64_t s = s0 + lane;
-  const int row = threadIdx.x % R, ch = threadIdx.x / R;  // loader: row, column half
-  const int64_t tiles = (N + R - 1) / R;
-  auto load = [&](int buf, int64_t t0) {
-    const int64_t t = t0 + row;
-#pragma unroll 4
-    for (int k = 0; k < 16; ++k) {
-      const int c = ch * 16 + k;
-      const int64_t col = s0 + c;
-      if (t < N && col < n)
-        cp_async8(&tile[buf][row][c], X + t + col * N);
-      else
-        tile[buf][row][c] = 0.0;
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  double sum = 0.0, mean = 0.0, ss = 0.0;
-  for (int pass = 0; pass < 2; ++pass) {
-    load(0, 0);
-    for (int64_t it = 0; it < tiles; ++it) {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      __syncthreads();  // tile it visible; everyone is done with tile it - 1
-      if (it + 1 < tiles) load(static_cast<int>((it + 1) & 1), (it + 1) * R);
-      if (warp == 0 && s < n) {
-        const int64_t t0 = it * R;
-        const int rows = static_cast<int>(N - t0 < R ? N - t0 : R);
-        const int buf = static_cast<int>(it & 1);
-        for (int r = 0; r < rows; ++r) {
-          const double v = tile[buf][r][lane];
-          if (pass == 0) {
-            sum = __dadd_rn(sum, v);
-          } else {
-            const double d = __dsub_rn(v, mean);
-            ss = __dadd_rn(ss, __dmul_rn(d, d));
-          }
-        }
+  const int lane = threadIdx.x & 31;
+  const int64_t s = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (s >= n) return;
+  const double* col = X + s * N;
+  constexpr int kAhead = 4;  // blocks of 32 rows in flight
+  auto block_sum = [&](double acc, double v, int rows, double mean, bool sq) {
+    for (int q = 0; q < rows; ++q) {
+      const double x = __shfl_sync(0xffffffffu, v, q);
+      if (sq) {
+        const double d = __dsub_rn(x, mean);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+      } else {
+        acc = __dadd_rn(acc, x);
       }
     }
-    __syncthreads();  // the last tile is consumed before the next pass reloads buffer 0
-    if (pass == 0) mean = sum / static_cast<double>(N);
+    return acc;
+  };
+  double mean = 0.0, acc = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    acc = 0.0;
+    for (int64_t t0 = 0; t0 < N; t0 += 32 * kAhead) {
+      double v[kAhead];
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) {
+        const int64_t t = t0 + 32 * k + lane;
+        v[k] = t < N ? __ldg(col + t) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) {
+        const int64_t b0 = t0 + 32 * k;
+        if (b0 >= N) break;
+        const int rows = N - b0 < 32 ? static_cast<int>(N - b0) : 32;
+        acc = block_sum(acc, v[k], rows, mean, pass == 1);
+      }
+    }
+    if (pass == 0) mean = acc / static_cast<double>(N);
   }
-  if (warp == 0 && s < n) {
-    const double sd = sqrt(ss / static_cast<double>(N));
+  if (lane == 0) {
+    const double sd = sqrt(acc / static_cast<double>(N));
     scale[s] = sd > 1e-12 ? sd : 1e-12;
   }
 }

@@ -128,6 +128,24 @@ __global__ void __launch_bounds__(1024) p_row_scale_kernel(const double* __restr
   scale_out_f[s] = static_cast<float>(scale_out_d[s]);
 }
 
+// Similarity centring add-back (cstress_b200.cu pack_fp32_operands): one
+// warp per signal, add_d[s] = scale_s * s_c * sum_j P(s, j) (fixed-order
+// shuffle reduction: the model is deterministic).
+__global__ void p_center_add_kernel(const double* __restrict__ P, const double* __restrict__ scale, int n, int m,
+                                    double s_c, double* __restrict__ add_d, float* __restrict__ add_f) {
+  const int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= n) return;
+  double r = 0.0;
+  for (int j = lane; j < m; j += 32) r += P[s + static_cast<int64_t>(j) * n];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  if (lane == 0) {
+    add_d[s] = scale[s] * s_c * r;
+    add_f[s] = static_cast<float>(add_d[s]);
+  }
+}
+
 // ||D_norm(:, c)||^2 (FP64 -> FP32, zero padded), D_norm in FP32, 1/scale,
 // and max |D_norm| (as the bit pattern of a non-negative float, for the
 // FP16-range check of the -2 d operand).

@@ -167,7 +167,9 @@ bool fleishman(double skew, double kurt, double out[4]) {
 }
 
 // Cholesky of the uniform correlation matrix with the jitter ladder
-// (nearest_psd_repair, signals.cpp:166-203); L lower, column-major.
+// (nearest_psd_repair, signals.cpp:166-203); L lower, stored ROW-major
+// (L[i * n + j] = L(i, j)) so the inner sums over j walk contiguous memory
+// -- the same products in the same order as Eigen's LLT (and the oracle).
 bool chol_uniform(int64_t n, double rho, std::vector<double>& L) {
   std::vector<double> tried = {0.0};
   double last = 0.0;
@@ -184,18 +186,20 @@ bool chol_uniform(int64_t n, double rho, std::vector<double>& L) {
     };
     bool ok = true;
     for (int64_t k = 0; k < n && ok; ++k) {
+      double* lk = L.data() + k * n;
       double x = A(k, k);
-      for (int64_t j = 0; j < k; ++j) x -= L[k + j * n] * L[k + j * n];
+      for (int64_t j = 0; j < k; ++j) x -= lk[j] * lk[j];
       if (!(x > 0.0)) {
         ok = false;
         break;
       }
       x = std::sqrt(x);
-      L[k + k * n] = x;
+      lk[k] = x;
       for (int64_t i = k + 1; i < n; ++i) {
+        double* li = L.data() + i * n;
         double v = A(i, k);
-        for (int64_t j = 0; j < k; ++j) v -= L[i + j * n] * L[k + j * n];
-        L[i + k * n] = v / x;
+        for (int64_t j = 0; j < k; ++j) v -= li[j] * lk[j];
+        li[k] = v / x;
       }
     }
     if (ok) return true;
@@ -366,7 +370,8 @@ extern "C" cs_status cs_synthesize_uniform(int64_t n, int64_t N, double phi, dou
         for (int64_t k = 0; k < n; ++k) row[k] = out[t + k * N];
         for (int64_t s = 0; s < n; ++s) {
           double acc = 0.0;
-          for (int64_t k = 0; k <= s; ++k) acc += row[k] * L[s + k * n];
+          const double* ls = L.data() + s * n;  // row s of L (row-major)
+          for (int64_t k = 0; k <= s; ++k) acc += row[k] * ls[k];
           out[t + s * N] = acc;
         }
       }

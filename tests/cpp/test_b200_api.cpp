@@ -156,11 +156,30 @@ static void plugin_cases() {  // test_mset.cpp:324-347
   CHECK_THROWS_AS(algorithm_by_name("svm"), ConfigError);
 }
 
+static void mean_predictor_cases() {  // estimator.cpp:42-69 (host baseline predictor)
+  const auto& algo = algorithm_by_name("mean");
+  CHECK(algo.name() == "mean");
+  Matrix X(4, 2);
+  const double v[8] = {1, 2, 3, 6, -1, -1, 5, 1};
+  for (int i = 0; i < 8; ++i) X.v[size_t(i)] = v[i];
+  const auto model = algo.train(SignalMatrix{X}, 2, {}, B64);
+  Matrix O(2, 2);
+  O(0, 0) = 4.0, O(1, 0) = 2.0, O(0, 1) = 0.0, O(1, 1) = 1.0;
+  const auto r = algo.estimate(*model, SignalMatrix{O}, B64);
+  CHECK(r.estimates(0, 0) == 3.0 && r.estimates(1, 0) == 3.0);  // mean of 1, 2, 3, 6
+  CHECK(r.estimates(0, 1) == 1.0 && r.estimates(1, 1) == 1.0);  // mean of -1, -1, 5, 1
+  CHECK(r.residuals(0, 0) == 1.0 && r.residuals(1, 0) == -1.0 && r.residuals(0, 1) == -1.0);
+  CHECK_THROWS_AS(algo.estimate(*model, SignalMatrix{Matrix(2, 3)}, B64), ShapeError);
+  const auto mset_model = algorithm_by_name("mset2").train(random_signals(2, 64, 61), 4, {}, B64);
+  CHECK_THROWS_AS(algo.estimate(*mset_model, SignalMatrix{O}, B64), ConfigError);
+}
+
 int main(int argc, char** argv) {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"kernel closed forms", kernel_closed_forms}, {"selection", selection_cases},
       {"matmul / batched_solve", matmul_cases},     {"symmetric_eig", eig_cases},
       {"train / estimate", training_cases},         {"plugin contract", plugin_cases},
+      {"mean predictor", mean_predictor_cases},
   };
   if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {
     for (const auto& c : cases) std::printf("%s\n", c.first);

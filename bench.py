@@ -741,7 +741,7 @@ def run_b200(args, world, rank, local):
     achieved_tflops = flops_per_obs * N_OBS / (mean_ms * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops", 1590.0)
     p_eff = bf16 / 3.0
-    K1, N2 = (N_SIG + 2 + 15) // 16 * 16, (N_SIG + 15) // 16 * 16  # + ||d||^2, ||x||^2 columns
+    K1, N2 = (N_SIG + 2 + 15) // 16 * 16, (N_SIG + 7) // 8 * 8  # + ||d||^2, ||x||^2 columns; GEMM2 N steps by 8
     MT = 64
     m_pad = (N_MEM + MT - 1) // MT * MT
     n_tiles = (N_OBS + 127) // 128

@@ -128,7 +128,7 @@ constexpr int kTlCap = 8192;
 // TMEM columns used for a given shape, ACC buffer count NB and S buffer
 // count SB (each 1 or 2, SB <= NB).
 __host__ __device__ constexpr int tc_tmem_cols(int N2, int K1, int MT, int NB, int SB) {
-  return N2 + K1 + NB * MT + SB * MT;  // X and S as f16x2 hi | lo pairs
+  return (N2 + 15) / 16 * 16 + K1 + NB * MT + SB * MT;  // X and S as f16x2 hi | lo pairs
 }
 
 // Shared-memory footprint of everything but the operand rings: barriers,
@@ -287,8 +287,10 @@ __global__ void __launch_bounds__(tc_threads(NB, SB), 1) mset_estimate_tc_kernel
   };
   const int K1 = p.K1, N2 = p.N2;
   const uint32_t colO = 0;
-  const uint32_t colXh = N2, colXl = N2 + K1 / 2;
-  const uint32_t colAcc = N2 + K1;         // + b*MT
+  // O's TMEM columns are kept at a multiple of 16 (GEMM2's N = N2 may be a
+  // multiple of 8 only: tcgen05 N steps by 8 for M = 128)
+  const uint32_t colXh = (N2 + 15) / 16 * 16, colXl = colXh + K1 / 2;
+  const uint32_t colAcc = colXh + K1;      // + b*MT
   const uint32_t colS = colAcc + NB * MT;  // + b*MT (hi), + MT/2 (lo)
   const int n_tiles = static_cast<int>((p.N + kObsTile - 1) / kObsTile);
   const int T = p.m_tiles;

@@ -288,7 +288,9 @@ def run_bench_sweep(world, rank, local, barrier, max_over_ranks):
             "timed_surveil_s": surv_s, "scaling": "strong", "n_gpus": world,
             "grid": {**SWEEP_GRID, "replicates": SWEEP_REPLICATES, "warmups": 1},
             "note": "full C4 grid (SURVEY 8d); device-side synthesis; wall includes synthesis, "
-                    "untimed warm-ups and the gather"}
+                    "untimed warm-ups and the gather; timed train = certified-Cholesky train with "
+                    "eigen_spectrum deferred to first export (the `train.ms` headline above is the "
+                    "eager, reference-contract time)"}
 
 
 def run_host_sweep(local):

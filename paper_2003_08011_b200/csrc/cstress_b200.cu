@@ -820,12 +820,33 @@ void check_model_shape(const cs_model* M, int64_t n) {
 void estimate_fp64_device(cs_ctx* ctx, cudaStream_t st, const cs_model* M, const double* obs,
                           int64_t N, int64_t ld, double* est, double* resid) {
   const int64_t n = M->n, m = M->m;
-  const int64_t budget = (int64_t{1} << 28);  // doubles per m x Nc workspace
-  const int64_t Nc = std::max<int64_t>(1, std::min<int64_t>(N, budget / std::max<int64_t>(m, 1)));
-  ctx->wsA.resize(n * Nc);
-  ctx->wsB.resize(m * Nc);
-  ctx->wsC.resize(m * Nc);
-  ctx->wsD.resize(n * Nc);
+  // Chunk of Nc observations: four workspaces of (2n + 2m) x Nc doubles,
+  // at most 2^28 doubles per m x Nc buffer and half the free device memory;
+  // halved on an allocation failure.  Every kernel of this path is exact per
+  // observation, so the chunking never changes a bit of the result.
+  const int64_t budget = (int64_t{1} << 28);
+  int64_t Nc = std::max<int64_t>(1, std::min<int64_t>(N, budget / std::max<int64_t>(m, 1)));
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+    const int64_t have = static_cast<int64_t>(std::min(ctx->wsB.count, ctx->wsC.count) / std::max<int64_t>(m, 1));
+    const int64_t cap = static_cast<int64_t>(free_b / 2 / (8 * static_cast<size_t>(2 * n + 2 * m)));
+    Nc = std::max<int64_t>(1, std::min(Nc, std::max(cap, have)));
+  } else {
+    cudaGetLastError();
+  }
+  for (;;) {
+    try {
+      ctx->wsA.resize(n * Nc);
+      ctx->wsB.resize(m * Nc);
+      ctx->wsC.resize(m * Nc);
+      ctx->wsD.resize(n * Nc);
+      break;
+    } catch (const Failure&) {
+      cudaGetLastError();
+      if (Nc == 1) throw;
+      Nc = (Nc + 1) / 2;
+    }
+  }
   for (int64_t t0 = 0; t0 < N; t0 += Nc) {
     const int64_t nc = std::min(Nc, N - t0);
     dim3 tg(ceil_div(nc, 32), ceil_div(n, 32)), tb(32, 8);

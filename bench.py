@@ -158,6 +158,20 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
 
 
+SUSTAINED_NOTE = ("P_eff = measured dense bf16 SUSTAINED (MEASURED_PEAKS.json bf16_tflops_sustained; the "
+                  "passes run back to back for seconds, where the clock settles at ~1.35 GHz) / 3: 3xFP16 "
+                  "split products; frac_vs_burst_peak uses the burst figure")
+
+
+def sustained_p_eff():
+    """(sustained, burst) 3xFP16 ceilings: long back-to-back passes (C3, C5')
+    are judged against the sustained measured bf16 rate, single short
+    launches (the C2 step) against the burst rate (B200_PROFILING.md)."""
+    peaks = load_peaks()
+    burst = peaks.get("bf16_tflops", 1590.0)
+    return peaks.get("bf16_tflops_sustained", burst) / 3, burst / 3
+
+
 def load_probe_peaks():
     """FP64 (DMMA, DFMA) and MUFU throughputs measured on this pool by
     tools/peaks_probe.cu (profiles/peaks_probe.json)."""
@@ -412,14 +426,14 @@ def run_large(local, n, N, m, workload, passes=5, e2e_obs=0, cpu_obs=0):
     ok = bool(torch.isfinite(est).all()) and bool(torch.allclose(res, obs - est))
     ms = statistics.median(ms_list)
     flops = 4.0 * n * m * N
-    peaks = load_peaks()
-    p_eff = peaks.get("bf16_tflops", 1590.0) / 3
+    p_eff, p_burst = sustained_p_eff()
+    tf = flops / (ms * 1e-3) / 1e12
     out = {"workload": workload, "n_signals": n, "n_observations": N, "n_memory": m,
            "obs_per_s": N / (ms * 1e-3), "ms_per_pass": ms, "passes": passes,
-           "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
-           "roofline": {"bound": "tensor", "peak": p_eff, "unit": "TFLOP/s",
-                        "frac": flops / (ms * 1e-3) / 1e12 / p_eff,
-                        "peak_note": "measured dense bf16 (MEASURED_PEAKS.json) / 3: 3xFP16 split products"},
+           "algorithmic_tflops": tf,
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": p_eff, "unit": "TFLOP/s",
+                        "frac": tf / p_eff, "frac_vs_burst_peak": tf / p_burst,
+                        "peak_note": SUSTAINED_NOTE},
            "kernels": "pack_obs + obs_sqnorm + gemm3x_f16_kernel<256,EpiSim> + gemm3x_f16_kernel<256,EpiOut> "
                       "per observation block",
            "train_ms": statistics.median(tt_eager) * 1e3, "train_ms_min": min(tt_eager) * 1e3,
@@ -545,7 +559,7 @@ def run_c5(args, world, rank, local, barrier, max_over_ranks):
         del model
         return None
     flops = 4.0 * n * m * C5_N
-    p_eff = load_peaks().get("bf16_tflops", 1590.0) / 3
+    p_eff, p_burst = sustained_p_eff()
     out.update(obs_per_s=C5_N / (ms_max * 1e-3), ms_estimate_max_over_ranks=ms_max,
                broadcast_ms=bcast_s * 1e3, model_wire_bytes=wire_bytes,
                collective="NCCL broadcast of the packed model (torch.distributed, %d ranks)" % world
@@ -556,9 +570,10 @@ def run_c5(args, world, rank, local, barrier, max_over_ranks):
                digest_note="sum of the FP32 words of all 10M x 4000 estimates (int64, wrapping): equal at "
                            "every GPU count when the sharded outputs are bitwise equal",
                algorithmic_tflops=flops / (ms_max * 1e-3) / 1e12,
-               roofline={"bound": "tensor", "peak": p_eff, "unit": "TFLOP/s",
-                         "frac": flops / (ms_max * 1e-3) / 1e12 / (p_eff * world),
-                         "peak_note": "measured dense bf16 (MEASURED_PEAKS.json) / 3 per GPU x n_gpus"},
+               roofline={"bound": "tensor", "achieved": flops / (ms_max * 1e-3) / 1e12, "peak": p_eff * world,
+                         "unit": "TFLOP/s", "frac": flops / (ms_max * 1e-3) / 1e12 / (p_eff * world),
+                         "frac_vs_burst_peak": flops / (ms_max * 1e-3) / 1e12 / (p_burst * world),
+                         "peak_note": SUSTAINED_NOTE + " (per GPU x n_gpus)"},
                kernels="pack_obs + obs_sqnorm + gemm3x_f16_kernel<256,EpiSim> + gemm3x_f16_kernel<256,EpiOut> "
                        "per observation block")
     del model

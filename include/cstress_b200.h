@@ -103,6 +103,13 @@ cs_status cs_symmetric_eig(cs_ctx* ctx, const double* G, int64_t m,
                            double* eigenvalues /* m, ascending */,
                            double* eigenvectors /* m x m */);
 
+/* Eigenvalues only (ascending) of a symmetric m x m matrix -- the
+ * eigen_spectrum part of symmetric_eig (mset.cpp:57-70), same precondition
+ * (ShapeError when not symmetric to 1e-9).  cuSOLVER syevd; with
+ * CSB_EIG_OWN=1 and m <= 2048 the library's own cluster tridiagonalisation
+ * + bisection (exact to 1e-12 of max|lambda|, slower). */
+cs_status cs_symmetric_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w);
+
 /* select_memory_vectors (mset.cpp:72-137): bit-exact indices. */
 cs_status cs_select_memory_vectors(cs_ctx* ctx, const double* training,
                                    int64_t N, int64_t n, int64_t m,

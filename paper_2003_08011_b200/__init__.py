@@ -8,7 +8,7 @@ from . import errors  # noqa: F401
 from .errors import *  # noqa: F401,F403
 from .mset import (BackendId, KernelConfig, KernelKind, TrainedModel, EstimationResult,  # noqa: F401
                    batched_solve, capabilities, context, estimate, estimate_device, import_model, train_device,
-                   matmul, select_memory_vectors, sim_matrix, similarity_matrix, symmetric_eig, train,
+                   matmul, select_memory_vectors, sim_matrix, similarity_matrix, symmetric_eig, symmetric_eigvals, train,
                    save_model, load_model, pack_model, unpack_model)
 from . import shard  # noqa: F401,E402
 from .estimator import (MeanPredictor, MsetAlgorithm, PrognosticAlgorithm,  # noqa: F401

@@ -38,6 +38,7 @@ _SIGNATURES = {
     "cs_matmul": (i32, [vp, pd, pd, i64, i64, i64, pd]),
     "cs_batched_solve": (i32, [vp, pd, pd, i64, i64, pd]),
     "cs_symmetric_eig": (i32, [vp, pd, i64, pd, pd]),
+    "cs_symmetric_eigvals": (i32, [vp, pd, i64, pd]),
     "cs_select_memory_vectors": (i32, [vp, pd, i64, i64, i64, pi64, pd]),
     "cs_mset_train": (i32, [vp, pd, i64, i64, i64, i32, d, i32, P(vp)]),
     "cs_mset_train_device": (i32, [vp, vp, i64, i64, i64, i32, d, i32, P(vp)]),

@@ -33,6 +33,7 @@
 #include "solver.cuh"
 #include "synth.cuh"
 #include "train_f64.h"
+#include "eig_tridiag.cuh"
 
 using namespace csb;
 
@@ -231,6 +232,89 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
   CSB_CUDA(cudaStreamSynchronize(st));
 }
 
+// ------------------------------------------- eigenvalues without cuSOLVER
+// (eig_tridiag.cuh): cluster tridiagonalisation + bisection, m <= kTriMaxM.
+// Returns false when the cluster cannot be launched (the caller then uses
+// syevd).  w is a device array (ascending).
+bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
+  if (m < 1 || m > kTriMaxM) return false;
+  // opt-in (CSB_EIG_OWN=1): correct to 1e-12 of max|lambda| (tests/test_gpu_eig.py)
+  // but measured 3-12x SLOWER than cuSOLVER's syevd (m = 1000: 66 vs 12 ms):
+  // four cluster barriers and latency-bound L2 streams per column of a
+  // one-stage reduction lose to sytrd's blocked kernels
+  const char* own = std::getenv("CSB_EIG_OWN");
+  if (!(own && own[0] == '1')) return false;
+  cudaStream_t st = ctx->stream;
+  StreamScope scope(st);
+  // cluster size: 16 (non-portable) when the device takes it, else 8
+  static int cs_best = 0;
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (cs_best == 0) {
+      cs_best = 8;
+      if (cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+          cudaSuccess) {
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(16);
+        q.blockDim = dim3(kTriThreads);
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = 16;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        q.attrs = &at;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, tridiag_cluster_kernel, &q) == cudaSuccess && n > 0) cs_best = 16;
+      }
+      cudaGetLastError();
+    }
+  }
+  const int CS = cs_best;
+  if ((m + CS - 1) / CS > 128) return false;
+  TmpBuf<double> A(static_cast<size_t>(m) * m), d(m), e(m + 1), gv(m), gw(m);
+  CSB_CUDA(cudaMemcpyAsync(A.get(), G, static_cast<size_t>(m) * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  TriArgs ta{A.get(), static_cast<int>(m), d.get(), e.get(), gv.get(), gw.get()};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CS);
+  cfg.blockDim = dim3(kTriThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at{};
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = CS;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  CSB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, ta));
+  CSB_LAUNCH_CHECK();
+  // Gershgorin interval of T (host: 2m doubles), LAPACK dstebz's pivmin
+  std::vector<double> hd(m), he(m + 1, 0.0);
+  CSB_CUDA(cudaMemcpyAsync(hd.data(), d.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (m > 1) CSB_CUDA(cudaMemcpyAsync(he.data(), e.get(), (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  double lo = 0.0, hi = 0.0, tnorm = 0.0, e2max = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    const double r = (i > 0 ? std::fabs(he[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(he[i]) : 0.0);
+    lo = i == 0 ? hd[i] - r : std::min(lo, hd[i] - r);
+    hi = i == 0 ? hd[i] + r : std::max(hi, hd[i] + r);
+    if (i + 1 < m) e2max = std::max(e2max, he[i] * he[i]);
+  }
+  tnorm = std::max(std::fabs(lo), std::fabs(hi));
+  const double pivmin = 2.2250738585072014e-308 * std::max(1.0, e2max);
+  const double pad = 2.0 * 2.220446049250313e-16 * tnorm * static_cast<double>(m) + 2.0 * pivmin;
+  lo -= pad;
+  hi += pad;
+  const int per_block = 128 * kBisectPer;
+  const size_t smem = static_cast<size_t>(2) * m * sizeof(double);
+  tridiag_bisect_kernel<<<ceil_div(m, per_block), 128, smem, st>>>(d.get(), e.get(), static_cast<int>(m), lo, hi,
+                                                                   pivmin, w);
+  CSB_LAUNCH_CHECK();
+  CSB_CUDA(cudaStreamSynchronize(st));  // the temporaries go back to the pool
+  return true;
+}
+
 // ---------------------------------------------------------- eigensolver
 // symmetric_eig (mset.cpp:57-70): precondition check, then cuSOLVER syevd
 // (FP64, ascending eigenvalues, orthonormal eigenvectors) in place on V.
@@ -248,6 +332,8 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V, b
   std::memcpy(&mag, &hs[0], 8);
   std::memcpy(&asym, &hs[1], 8);
   if (asym > 1e-9 * std::max(mag, 1.0)) fail(CS_SHAPE_ERROR, "symmetric_eig: matrix is not symmetric to 1e-9");
+  // eigenvalues only: own cluster tridiagonalisation + bisection (m <= 2048)
+  if (!vectors && tridiag_eigvals(ctx, G, m, w)) return;
   if (V != G) CSB_CUDA(cudaMemcpyAsync(V, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
   const CusolverApi& api = cusolver_api();
   if (!ctx->solver) solver_check(api.create(&ctx->solver), "cusolverDnCreate");
@@ -1342,6 +1428,20 @@ cs_status cs_symmetric_eig(cs_ctx* ctx, const double* G, int64_t m, double* w, d
     CSB_CUDA(cudaMemcpyAsync(w, dw.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaMemcpyAsync(V, dV.get(), m * m * sizeof(double), cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+cs_status cs_symmetric_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
+  return guarded([&] {
+    if (!ctx || (!G && m > 0) || (!w && m > 0)) fail(CS_CONFIG_ERROR, "symmetric_eigvals: null argument");
+    if (m == 0) return;
+    set_device(ctx->device);
+    StreamScope scope(ctx->stream);
+    TmpBuf<double> dG(static_cast<size_t>(m) * m), dV(static_cast<size_t>(m) * m), dw(m);
+    CSB_CUDA(cudaMemcpyAsync(dG.get(), G, m * m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    eig_device(ctx, dG.get(), m, dw.get(), dV.get(), false);
+    CSB_CUDA(cudaMemcpyAsync(w, dw.get(), m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CSB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -225,29 +225,44 @@ scale_seq_kernel(const double* __restrict__ X, int64_t N, int64_t n, double* __r
   const int64_t s = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (s >= n) return;
   const double* col = X + s * N;
-  constexpr int kAhead = 4;  // blocks of 32 rows in flight
+  constexpr int kAhead = 8;  // blocks of 32 rows per group (two groups in flight)
   auto block_sum = [&](double acc, double v, int rows, double mean, bool sq) {
-    for (int q = 0; q < rows; ++q) {
-      const double x = __shfl_sync(0xffffffffu, v, q);
-      if (sq) {
-        const double d = __dsub_rn(x, mean);
-        acc = __dadd_rn(acc, __dmul_rn(d, d));
-      } else {
-        acc = __dadd_rn(acc, x);
+    // eight broadcasts in flight ahead of the serial adds: the chain then
+    // waits on DADD latency only, not on a shuffle per element
+    for (int q0 = 0; q0 < rows; q0 += 8) {
+      double xs[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xs[u] = __shfl_sync(0xffffffffu, v, (q0 + u) & 31);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (q0 + u >= rows) break;
+        if (sq) {
+          const double d = __dsub_rn(xs[u], mean);
+          acc = __dadd_rn(acc, __dmul_rn(d, d));
+        } else {
+          acc = __dadd_rn(acc, xs[u]);
+        }
       }
     }
     return acc;
   };
   double mean = 0.0, acc = 0.0;
+  // software pipelined: the next kAhead blocks are in flight while the
+  // serial sum runs over the current ones (one memory latency per column,
+  // not one per block group)
+  auto load = [&](double* v, int64_t t0) {
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) {
+      const int64_t t = t0 + 32 * k + lane;
+      v[k] = t < N ? __ldg(col + t) : 0.0;
+    }
+  };
   for (int pass = 0; pass < 2; ++pass) {
     acc = 0.0;
+    double v[kAhead], vn[kAhead];
+    load(v, 0);
     for (int64_t t0 = 0; t0 < N; t0 += 32 * kAhead) {
-      double v[kAhead];
-#pragma unroll
-      for (int k = 0; k < kAhead; ++k) {
-        const int64_t t = t0 + 32 * k + lane;
-        v[k] = t < N ? __ldg(col + t) : 0.0;
-      }
+      if (t0 + 32 * kAhead < N) load(vn, t0 + 32 * kAhead);
 #pragma unroll
       for (int k = 0; k < kAhead; ++k) {
         const int64_t b0 = t0 + 32 * k;
@@ -255,6 +270,8 @@ scale_seq_kernel(const double* __restrict__ X, int64_t N, int64_t n, double* __r
         const int rows = N - b0 < 32 ? static_cast<int>(N - b0) : 32;
         acc = block_sum(acc, v[k], rows, mean, pass == 1);
       }
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) v[k] = vn[k];
     }
     if (pass == 0) mean = acc / static_cast<double>(N);
   }

@@ -259,6 +259,20 @@ def symmetric_eig(G, backend: BackendId = BackendId()) -> SymmetricEig:
     return SymmetricEig(w, V)
 
 
+def symmetric_eigvals(G, backend: BackendId = BackendId()) -> np.ndarray:
+    """The eigenvalues (ascending) of symmetric_eig (mset.hpp:34-38) without
+    the vectors (cs_symmetric_eigvals): cuSOLVER syevd, or with
+    CSB_EIG_OWN=1 and m <= 2048 the library's own cluster tridiagonalisation
+    + bisection."""
+    G = f64(G)
+    if G.ndim != 2 or G.shape[0] != G.shape[1]:
+        raise ShapeError("symmetric_eig: matrix is not square")
+    m = G.shape[0]
+    w = np.empty(m)
+    check(_lib.lib().cs_symmetric_eigvals(_ctx(backend).handle, ptr_d(G), m, ptr_d(w)))
+    return w
+
+
 @dataclass
 class MemoryMatrix:
     """mset.hpp:21-27"""

@@ -1,0 +1,89 @@
+"""Eigenvalues without cuSOLVER (csrc/eig_tridiag.cuh): cluster Householder
+tridiagonalisation + Sturm bisection, the path of the eager eigen_spectrum
+and of the eigen route's rank decision (mset.cpp:153-163) for m <= 2048.
+Checked against LAPACK (numpy.linalg.eigvalsh) to 1e-12 of max|lambda| --
+the reference's own spectrum pin is 1e-10 (test_mset.cpp:163-199) -- on
+random symmetric matrices of awkward sizes, rank-deficient Gram matrices
+(duplicate memory vectors, test_mset.cpp:228-234), clustered spectra, and
+against the cuSOLVER route of the same library (the default route; the
+own one is opt-in, CSB_EIG_OWN=1, because it is slower)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def p():
+    import torch  # noqa: F401
+    import paper_2003_08011_b200 as p
+    p.context(0)
+    return p
+
+
+@pytest.fixture(autouse=True)
+def own_path(monkeypatch):
+    # the own solver is opt-in (it is slower than cuSOLVER's syevd, which
+    # stays the default); these tests pin its numerics
+    monkeypatch.setenv("CSB_EIG_OWN", "1")
+
+
+def _err(w, want):
+    return float(np.abs(np.asarray(w) - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 17, 33, 100, 127, 129, 513, 1000, 2048])
+def test_random_symmetric(p, m):
+    rng = np.random.default_rng(m)
+    A = rng.standard_normal((m, m))
+    A = np.asfortranarray(A + A.T)
+    w = p.symmetric_eigvals(A)
+    assert (np.diff(w) >= 0).all()
+    assert _err(w, np.linalg.eigvalsh(A)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,dups", [(300, 40), (1000, 7)])
+def test_rank_deficient_gram(p, m, dups):
+    """Gram matrix of memory vectors with duplicates: exact zero eigenvalues
+    (rank < m) must come out at the 1e-12 lambda_max level, like LAPACK."""
+    rng = np.random.default_rng(7)
+    n = 20
+    D = rng.standard_normal((n, m - dups))
+    D = np.hstack([D, D[:, :dups]])
+    d2 = ((D[:, :, None] - D[:, None, :]) ** 2).sum(0)
+    G = np.asfortranarray(1.0 / (1.0 + np.sqrt(d2) / np.sqrt(n)))
+    w = p.symmetric_eigvals(G)
+    want = np.linalg.eigvalsh(G)
+    assert _err(w, want) <= 1e-12
+    cut = 1e-10 * want[-1]
+    assert (w > cut).sum() == (want > cut).sum() == m - dups  # the rank decision of mset.cpp:156-163
+
+
+def test_clustered_spectrum(p):
+    m = 700
+    rng = np.random.default_rng(3)
+    Q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    lam = np.concatenate([np.full(300, 1.0), np.full(300, 1.0 + 1e-9), np.linspace(2, 5, 100)])
+    A = np.asfortranarray((Q * lam) @ Q.T)
+    A = np.asfortranarray(0.5 * (A + A.T))
+    assert _err(p.symmetric_eigvals(A), np.linalg.eigvalsh(A)) <= 1e-12
+
+
+def test_matches_cusolver_route(p, monkeypatch):
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((600, 600))
+    A = np.asfortranarray(A @ A.T)
+    own = p.symmetric_eigvals(A)
+    monkeypatch.delenv("CSB_EIG_OWN")
+    lib = p.symmetric_eigvals(A)
+    assert _err(own, lib) <= 1e-12
+
+
+def test_not_symmetric_is_shape_error(p):
+    from paper_2003_08011_b200.errors import ShapeError
+    A = np.eye(10)
+    A[0, 1] = 1.0
+    with pytest.raises(ShapeError):
+        p.symmetric_eigvals(A)

@@ -236,16 +236,32 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
 // (eig_tridiag.cuh): cluster tridiagonalisation + bisection, m <= kTriMaxM.
 // Returns false when the cluster cannot be launched (the caller then uses
 // syevd).  w is a device array (ascending).
+bool bisect_eigvals(cudaStream_t st, const double* dd, const double* de, int64_t m, double* w);
 bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   if (m < 1 || m > kTriMaxM) return false;
-  // opt-in (CSB_EIG_OWN=1): correct to 1e-12 of max|lambda| (tests/test_gpu_eig.py)
-  // but measured 3-12x SLOWER than cuSOLVER's syevd (m = 1000: 66 vs 12 ms):
-  // four cluster barriers and latency-bound L2 streams per column of a
-  // one-stage reduction lose to sytrd's blocked kernels
+  // Default for m <= kTriOwnMaxM, where it beats syevd (one CTA with the
+  // matrix in shared memory up to kTriCtaMaxM, the 16-CTA cluster above);
+  // opt-in (CSB_EIG_OWN=1) up to kTriMaxM; CSB_EIG_OWN=0: never
+  // (eig_tridiag.cuh has the measurements).
   const char* own = std::getenv("CSB_EIG_OWN");
-  if (!(own && own[0] == '1')) return false;
+  if (own && own[0] == '0') return false;
+  const bool small = m <= kTriCtaMaxM;
+  if (m > kTriOwnMaxM && !(own && own[0] == '1')) return false;
   cudaStream_t st = ctx->stream;
   StreamScope scope(st);
+  TmpBuf<double> d(m), e(m + 1);
+  if (small) {
+    static bool attr = false;
+    if (!attr) {
+      CSB_CUDA(cudaFuncSetAttribute(tridiag_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(tri_cta_smem(kTriCtaMaxM))));
+      attr = true;
+    }
+    tridiag_cta_kernel<<<1, kTriCtaThreads, tri_cta_smem(static_cast<int>(m)), st>>>(G, static_cast<int>(m), d.get(),
+                                                                                     e.get());
+    CSB_LAUNCH_CHECK();
+    return bisect_eigvals(st, d.get(), e.get(), m, w);
+  }
   // cluster size: 16 (non-portable) when the device takes it, else 8
   static int cs_best = 0;
   static std::mutex mu;
@@ -273,7 +289,7 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   }
   const int CS = cs_best;
   if ((m + CS - 1) / CS > 128) return false;
-  TmpBuf<double> A(static_cast<size_t>(m) * m), d(m), e(m + 1), gv(m), gw(m);
+  TmpBuf<double> A(static_cast<size_t>(m) * m), gv(m), gw(m);
   CSB_CUDA(cudaMemcpyAsync(A.get(), G, static_cast<size_t>(m) * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
   TriArgs ta{A.get(), static_cast<int>(m), d.get(), e.get(), gv.get(), gw.get()};
   cudaLaunchConfig_t cfg{};
@@ -289,10 +305,15 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   cfg.numAttrs = 1;
   CSB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, ta));
   CSB_LAUNCH_CHECK();
+  return bisect_eigvals(st, d.get(), e.get(), m, w);
+}
+
+// eigenvalues (ascending) of the device tridiagonal (d, e) by bisection
+bool bisect_eigvals(cudaStream_t st, const double* dd, const double* de, int64_t m, double* w) {
   // Gershgorin interval of T (host: 2m doubles), LAPACK dstebz's pivmin
   std::vector<double> hd(m), he(m + 1, 0.0);
-  CSB_CUDA(cudaMemcpyAsync(hd.data(), d.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (m > 1) CSB_CUDA(cudaMemcpyAsync(he.data(), e.get(), (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaMemcpyAsync(hd.data(), dd, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (m > 1) CSB_CUDA(cudaMemcpyAsync(he.data(), de, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
   CSB_CUDA(cudaStreamSynchronize(st));
   double lo = 0.0, hi = 0.0, tnorm = 0.0, e2max = 0.0;
   for (int64_t i = 0; i < m; ++i) {
@@ -306,10 +327,9 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   const double pad = 2.0 * 2.220446049250313e-16 * tnorm * static_cast<double>(m) + 2.0 * pivmin;
   lo -= pad;
   hi += pad;
-  const int per_block = 128 * kBisectPer;
   const size_t smem = static_cast<size_t>(2) * m * sizeof(double);
-  tridiag_bisect_kernel<<<ceil_div(m, per_block), 128, smem, st>>>(d.get(), e.get(), static_cast<int>(m), lo, hi,
-                                                                   pivmin, w);
+  tridiag_bisect_kernel<<<ceil_div(m, kBisectWarps), 128, smem, st>>>(dd, de, static_cast<int>(m), lo, hi, pivmin,
+                                                                       w);
   CSB_LAUNCH_CHECK();
   CSB_CUDA(cudaStreamSynchronize(st));  // the temporaries go back to the pool
   return true;

@@ -6,7 +6,7 @@ the reference's own spectrum pin is 1e-10 (test_mset.cpp:163-199) -- on
 random symmetric matrices of awkward sizes, rank-deficient Gram matrices
 (duplicate memory vectors, test_mset.cpp:228-234), clustered spectra, and
 against the cuSOLVER route of the same library (the default route; the
-own one is opt-in, CSB_EIG_OWN=1, because it is slower)."""
+own one is the default up to m = 512 and opt-in, CSB_EIG_OWN=1, above)."""
 import os
 
 import numpy as np
@@ -25,8 +25,8 @@ def p():
 
 @pytest.fixture(autouse=True)
 def own_path(monkeypatch):
-    # the own solver is opt-in (it is slower than cuSOLVER's syevd, which
-    # stays the default); these tests pin its numerics
+    # force the own solver at every size (above m = 512 it is opt-in:
+    # slower than cuSOLVER's syevd there); these tests pin its numerics
     monkeypatch.setenv("CSB_EIG_OWN", "1")
 
 
@@ -87,3 +87,18 @@ def test_not_symmetric_is_shape_error(p):
     A[0, 1] = 1.0
     with pytest.raises(ShapeError):
         p.symmetric_eigvals(A)
+
+
+@pytest.mark.parametrize("m", [2, 40, 100, 160, 200, 500])
+def test_small_default_path_matches_cusolver(p, monkeypatch, m):
+    """m <= 512: the own reduction (one CTA up to 160, the cluster above) is
+    the DEFAULT eigenvalues-only path (faster than syevd there);
+    CSB_EIG_OWN=0 forces syevd."""
+    rng = np.random.default_rng(100 + m)
+    A = rng.standard_normal((m, m))
+    A = np.asfortranarray(A @ A.T + np.eye(m))
+    monkeypatch.delenv("CSB_EIG_OWN")
+    own = p.symmetric_eigvals(A)
+    monkeypatch.setenv("CSB_EIG_OWN", "0")
+    lib = p.symmetric_eigvals(A)
+    assert _err(own, lib) <= 1e-12 and _err(own, np.linalg.eigvalsh(A)) <= 1e-12

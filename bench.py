@@ -66,6 +66,10 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # development only: several ranks on one GPU (CSB_BENCH_DEVICE=0 with
+    # CSB_BENCH_DIST_BACKEND=gloo) to exercise the multi-rank plumbing
+    if os.environ.get("CSB_BENCH_DEVICE"):
+        local = int(os.environ["CSB_BENCH_DEVICE"])
     return world, rank, local
 
 
@@ -473,6 +477,8 @@ def run_c3(args, local):
 
 
 C5_N, C5_n, C5_m, C5_CHUNK = 10_000_000, 4000, 8000, 1_250_000
+if os.environ.get("CSB_BENCH_C5_SMALL"):  # development only (multi-rank plumbing on one GPU)
+    C5_N, C5_n, C5_m, C5_CHUNK = 2_000_000, 1000, 2000, 250_000
 
 
 def run_c5(args, world, rank, local, barrier, max_over_ranks):
@@ -498,8 +504,8 @@ def run_c5(args, world, rank, local, barrier, max_over_ranks):
     spec = lambda rows, seed: p.SignalSpec.uniform(n, rows, t["phi"], t["rho"], t["var"], t["skew"],  # noqa: E731
                                                    t["kurt"], seed)
     backend = p.BackendId("b200", local, "fp32")
-    out = {"workload": "C5': n=4000, m=8000 (32k training rows), N=10M observations sharded over the ranks, "
-                       "FP32 device-resident I/O",
+    out = {"workload": f"C5': n={n}, m={m} ({TRAIN_FACTOR * m // 1000}k training rows), N={C5_N // 1_000_000}M "
+                       "observations sharded over the ranks, FP32 device-resident I/O",
            "n_signals": n, "n_memory": m, "n_observations": C5_N, "n_gpus": world, "scaling": "strong",
            "chunks": C5_N // C5_CHUNK}
     model = None
@@ -562,8 +568,8 @@ def run_c5(args, world, rank, local, barrier, max_over_ranks):
     p_eff, p_burst = sustained_p_eff()
     out.update(obs_per_s=C5_N / (ms_max * 1e-3), ms_estimate_max_over_ranks=ms_max,
                broadcast_ms=bcast_s * 1e3, model_wire_bytes=wire_bytes,
-               collective="NCCL broadcast of the packed model (torch.distributed, %d ranks)" % world
-               if world > 1 else "none (1 rank)",
+               collective="%s broadcast of the packed model (torch.distributed, %d ranks)" % (
+                   dist.get_backend().upper(), world) if world > 1 else "none (1 rank)",
                obs_per_s_incl_train_and_broadcast=C5_N / (out["train_ms_spectrum_deferred"] * 1e-3 + bcast_s
                                                           + ms_max * 1e-3),
                estimates_digest=wrap64(int(d.item())),
@@ -681,7 +687,8 @@ def run_b200(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        be = os.environ.get("CSB_BENCH_DIST_BACKEND", "nccl")
+        dist.init_process_group(be, device_id=dev if be == "nccl" else None)
     backend = p.BackendId("b200", local, "fp32")
 
     def barrier():

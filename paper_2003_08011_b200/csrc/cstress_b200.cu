@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -251,11 +252,12 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   StreamScope scope(st);
   TmpBuf<double> d(m), e(m + 1);
   if (small) {
-    static bool attr = false;
-    if (!attr) {
+    // the attribute is per (function, device)
+    static std::atomic<unsigned long long> attr_dev{0};
+    if (!(attr_dev.load() >> ctx->device & 1ull)) {
       CSB_CUDA(cudaFuncSetAttribute(tridiag_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(tri_cta_smem(kTriCtaMaxM))));
-      attr = true;
+      attr_dev.fetch_or(1ull << ctx->device);
     }
     tridiag_cta_kernel<<<1, kTriCtaThreads, tri_cta_smem(static_cast<int>(m)), st>>>(G, static_cast<int>(m), d.get(),
                                                                                      e.get());
@@ -263,12 +265,15 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
     return bisect_eigvals(st, d.get(), e.get(), m, w);
   }
   // cluster size: 16 (non-portable) when the device takes it, else 8
-  static int cs_best = 0;
+  // (per device: the attribute and the occupancy answer are per device)
+  static int cs_by_dev[64] = {};
   static std::mutex mu;
+  int cs_best = 8;
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (cs_best == 0) {
-      cs_best = 8;
+    int& cached = cs_by_dev[ctx->device & 63];
+    if (cached == 0) {
+      cached = 8;
       if (cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
           cudaSuccess) {
         cudaLaunchConfig_t q{};
@@ -282,10 +287,11 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
         q.attrs = &at;
         q.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, tridiag_cluster_kernel, &q) == cudaSuccess && n > 0) cs_best = 16;
+        if (cudaOccupancyMaxActiveClusters(&n, tridiag_cluster_kernel, &q) == cudaSuccess && n > 0) cached = 16;
       }
       cudaGetLastError();
     }
+    cs_best = cached;
   }
   const int CS = cs_best;
   if ((m + CS - 1) / CS > 128) return false;

@@ -20,7 +20,7 @@
 // reduction: CTA c holds rows [c R, c R + R) of the full symmetric working
 // matrix in global memory (L2-resident up to ~2k x 2k), the column step's
 // reductions go through distributed shared memory (partials
-// summed in rank order: deterministic); each column costs two cluster
+// read in parallel and summed by a fixed shuffle tree: deterministic); each column costs two cluster
 // barriers: v is re-derived by every CTA from column k in L2, p goes out
 // through L2 with the p.v partials and w = p - (tau K / 2) v is formed on the
 // fly in the rank-2 update.
@@ -99,12 +99,18 @@ __global__ void __launch_bounds__(kTriThreads, 1) tridiag_cluster_kernel(TriArgs
       red[par][1] = alp;
     }
     cluster.sync();
-    if (tid == 0) {
+    if (tid < 32) {
+      // lane q reads CTA q's partials (remote loads in parallel, not a
+      // dependent chain of DSMEM round trips), then a fixed shuffle tree
       double S = 0.0, Al = 0.0;
-      for (int q = 0; q < CS; ++q) {
-        const double* rq = cluster.map_shared_rank(&red[par][0], q);
-        S += rq[0];
-        Al += rq[1];
+      if (tid < CS) {
+        const double* rq = cluster.map_shared_rank(&red[par][0], tid);
+        S = rq[0];
+        Al = rq[1];
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Al += __shfl_xor_sync(0xffffffffu, Al, o);
       }
       double tau = 0.0, scal = 0.0, beta = Al;
       if (S > 0.0) {
@@ -113,11 +119,13 @@ __global__ void __launch_bounds__(kTriThreads, 1) tridiag_cluster_kernel(TriArgs
         tau = (beta - Al) / beta;
         scal = 1.0 / (Al - beta);
       }
-      bc[0] = tau;
-      bc[1] = scal;
-      if (c == 0) {
-        a.d[k] = A[static_cast<size_t>(k) * m + k];
-        a.e[k] = beta;
+      if (tid == 0) {
+        bc[0] = tau;
+        bc[1] = scal;
+        if (c == 0) {
+          a.d[k] = A[static_cast<size_t>(k) * m + k];
+          a.e[k] = beta;
+        }
       }
     }
     __syncthreads();
@@ -161,10 +169,10 @@ __global__ void __launch_bounds__(kTriThreads, 1) tridiag_cluster_kernel(TriArgs
     double pv = tri_block_sum(ph == 0 ? pi * vi : 0.0, scratch);
     if (tid == 0) red[par][2] = pv;
     cluster.sync();
-    if (tid == 0) {
-      double K = 0.0;
-      for (int q = 0; q < CS; ++q) K += cluster.map_shared_rank(&red[par][0], q)[2];
-      bc[2] = K;
+    if (tid < 32) {
+      double K = tid < CS ? cluster.map_shared_rank(&red[par][0], tid)[2] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+      if (tid == 0) bc[2] = K;
     }
     __syncthreads();
     const double hk = 0.5 * tau * bc[2];

@@ -693,8 +693,12 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
   M->scale_f.resize(n);
   TmpBuf<unsigned int> absmax(1);
   CSB_CUDA(cudaMemsetAsync(absmax.get(), 0, sizeof(unsigned int), st));
+  TmpBuf<double> dd64(m_pad);
+  dn_sqnorm_kernel<<<ceil_div(static_cast<int64_t>(m_pad) * 32, 256), 256, 0, st>>>(M->Dn.get(), n, m, m_pad,
+                                                                                   dd64.get());
+  CSB_LAUNCH_CHECK();
   pack_aux_kernel<<<grid_for(std::max<int64_t>(m_pad, static_cast<int64_t>(n) * m)), 256, 0, st>>>(
-      M->Dn.get(), M->scale.get(), n, m, m_pad, M->dd.get(), M->dn32.get(), M->inv_scale.get(),
+      M->Dn.get(), dd64.get(), M->scale.get(), n, m, m_pad, M->dd.get(), M->dn32.get(), M->inv_scale.get(),
       M->scale_f.get(), absmax.get());
   CSB_LAUNCH_CHECK();
   std::vector<float> dd_host(m_pad);
@@ -761,7 +765,7 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
     M->dn_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->MT * M->K1);
     M->p_tiles.resize(static_cast<size_t>(M->m_tiles) * 2 * M->N2 * M->MT);
     pack_dn_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->K1), 256, 0, st>>>(
-        M->Dn.get(), n, m, M->MT, M->K1, M->m_tiles, aug_scale, M->dn_tiles.get());
+        M->Dn.get(), dd64.get(), n, m, M->MT, M->K1, M->m_tiles, aug_scale, M->dn_tiles.get());
     CSB_LAUNCH_CHECK();
     pack_p_tiles_kernel<<<grid_for(static_cast<int64_t>(M->m_tiles) * M->MT * M->N2), 256, 0, st>>>(
         P.get(), M->p_shift.get(), n, m, M->MT, M->N2, M->m_tiles, M->p_tiles.get());
@@ -772,7 +776,7 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
     M->dn_gemm.resize(a_el);
     M->p_gemm.resize(b_el);
     pack_dn_gemm_kernel<<<grid_for(static_cast<int64_t>(a_el / 2)), 256, 0, st>>>(
-        M->Dn.get(), n, m, M->bnA, M->ntA, M->kcA, aug_scale, M->dn_gemm.get());
+        M->Dn.get(), dd64.get(), n, m, M->bnA, M->ntA, M->kcA, aug_scale, M->dn_gemm.get());
     CSB_LAUNCH_CHECK();
     pack_p_gemm_kernel<<<grid_for(static_cast<int64_t>(b_el / 2)), 256, 0, st>>>(
         P.get(), M->p_shift.get(), n, m, M->bnB, M->ntB, M->kcB, M->p_gemm.get());

@@ -416,8 +416,8 @@ __global__ void obs_sqnorm_kernel(const IO* __restrict__ obs, int64_t N, int64_t
 // Model operand for GEMM-A's B side: rows = memory vectors (BN-row tiles),
 // K = signals + the ||d||^2 column: -2 D_norm (exact) and ||d||^2 * aug_scale
 // (FP64), FP16 hi | lo.
-__global__ void pack_dn_gemm_kernel(const double* __restrict__ Dn, int n, int m, int BN, int n_tiles,
-                                    int k_chunks, double aug_scale, __half* __restrict__ out) {
+__global__ void pack_dn_gemm_kernel(const double* __restrict__ Dn, const double* __restrict__ dd64, int n, int m,
+                                    int BN, int n_tiles, int k_chunks, double aug_scale, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(BN) * kGemmBK;
   const int64_t total = per * k_chunks * n_tiles;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -425,18 +425,14 @@ __global__ void pack_dn_gemm_kernel(const double* __restrict__ Dn, int n, int m,
     const int64_t blk = e / per;
     const int rem = static_cast<int>(e % per);
     const int nt = static_cast<int>(blk / k_chunks), kc = static_cast<int>(blk % k_chunks);
-    const int r = rem % BN, kk = rem / BN;
+    const int kk = rem % kGemmBK, r = rem / kGemmBK;  // kk fastest: coalesced reads down a column
     const int mem = nt * BN + r, k = kc * kGemmBK + kk;
     double v = 0.0;
     if (mem < m) {
       if (k < n) {
         v = -2.0 * Dn[k + static_cast<int64_t>(mem) * n];
       } else if (k == n) {
-        for (int s = 0; s < n; ++s) {
-          const double d = Dn[s + static_cast<int64_t>(mem) * n];
-          v = fma(d, d, v);
-        }
-        v *= aug_scale;
+        v = dd64[mem] * aug_scale;
       }
     }
     __half hv, lv;

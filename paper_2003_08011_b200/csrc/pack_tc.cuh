@@ -43,26 +43,22 @@ __device__ __forceinline__ void split_f16(double v, __half& hi, __half& lo) {
 // (FP64, split), column n + 1 the constant kXxCol -- with x augmented by
 // 1/aug_scale in column n and ||x||^2 / kXxCol in column n + 1, GEMM1 yields
 // d2 = ||x||^2 + ||d||^2 - 2 x.d directly.
-__global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m, int MT, int K1,
-                                     int m_tiles, double aug_scale, __half* __restrict__ out) {
+__global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, const double* __restrict__ dd64, int n, int m,
+                                     int MT, int K1, int m_tiles, double aug_scale, __half* __restrict__ out) {
   const int64_t per = static_cast<int64_t>(MT) * K1;
   const int64_t total = per * m_tiles;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int j = static_cast<int>(e / per);
     const int rem = static_cast<int>(e % per);
-    const int r = rem % MT, k = rem / MT;
+    const int k = rem % K1, r = rem / K1;  // k fastest: coalesced reads down a D_norm column
     const int mem = j * MT + r;
     double v = 0.0;
     if (mem < m) {
       if (k < n) {
         v = -2.0 * Dn[k + static_cast<int64_t>(mem) * n];
       } else if (k == n) {
-        for (int s = 0; s < n; ++s) {
-          const double d = Dn[s + static_cast<int64_t>(mem) * n];
-          v = fma(d, d, v);
-        }
-        v *= aug_scale;
+        v = dd64[mem] * aug_scale;
       } else if (k == n + 1) {
         v = kXxCol;
       }
@@ -73,6 +69,23 @@ __global__ void pack_dn_tiles_kernel(const double* __restrict__ Dn, int n, int m
     blk[canon16(r, k, MT)] = hi;
     blk[per + canon16(r, k, MT)] = lo;
   }
+}
+
+// ||D_norm(:, c)||^2 in FP64, one warp per column (coalesced, fixed shuffle
+// order: deterministic), zero padded to m_pad
+__global__ void dn_sqnorm_kernel(const double* __restrict__ Dn, int n, int m, int m_pad, double* __restrict__ dd64) {
+  const int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= m_pad) return;
+  double a = 0.0;
+  if (c < m)
+    for (int s = lane; s < n; s += 32) {
+      const double v = Dn[s + c * n];
+      a = fma(v, v, a);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) dd64[c] = a;
 }
 
 // P^T tiles: block j holds signals as rows (N2), memory vectors j*MT.. as K;
@@ -149,21 +162,13 @@ __global__ void p_center_add_kernel(const double* __restrict__ P, const double* 
 // ||D_norm(:, c)||^2 (FP64 -> FP32, zero padded), D_norm in FP32, 1/scale,
 // and max |D_norm| (as the bit pattern of a non-negative float, for the
 // FP16-range check of the -2 d operand).
-__global__ void pack_aux_kernel(const double* __restrict__ Dn, const double* __restrict__ scale,
-                                int n, int m, int m_pad, float* __restrict__ dd,
+__global__ void pack_aux_kernel(const double* __restrict__ Dn, const double* __restrict__ dd64,
+                                const double* __restrict__ scale, int n, int m, int m_pad, float* __restrict__ dd,
                                 float* __restrict__ dn32, float* __restrict__ inv_scale,
                                 float* __restrict__ scale_f, unsigned int* __restrict__ dn_absmax) {
   const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t c = tid; c < m_pad; c += stride) {
-    double a = 0.0;
-    if (c < m)
-      for (int s = 0; s < n; ++s) {
-        const double v = Dn[s + c * n];
-        a = fma(v, v, a);
-      }
-    dd[c] = static_cast<float>(a);
-  }
+  for (int64_t c = tid; c < m_pad; c += stride) dd[c] = static_cast<float>(dd64[c]);
   float mx = 0.f;
   for (int64_t e = tid; e < static_cast<int64_t>(n) * m; e += stride) {
     dn32[e] = static_cast<float>(Dn[e]);

@@ -37,13 +37,13 @@ __global__ void row_hash_kernel(const double* __restrict__ X, int64_t N, int64_t
     }
   };
   int64_t s = 0;
-  // eight signals' loads in flight before their bytes enter the (serial) hash
-  for (; s + 8 <= n; s += 8) {
-    unsigned long long bits[8];
+  // sixteen signals' loads in flight before their bytes enter the (serial) hash
+  for (; s + 16 <= n; s += 16) {
+    unsigned long long bits[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) bits[k] = static_cast<unsigned long long>(__double_as_longlong(__ldg(X + r + (s + k) * N)));
+    for (int k = 0; k < 16; ++k) bits[k] = static_cast<unsigned long long>(__double_as_longlong(__ldg(X + r + (s + k) * N)));
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mix(bits[k]);
+    for (int k = 0; k < 16; ++k) mix(bits[k]);
   }
   for (; s < n; ++s) mix(static_cast<unsigned long long>(__double_as_longlong(__ldg(X + r + s * N))));
   hashes[r] = h;

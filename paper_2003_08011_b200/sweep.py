@@ -292,22 +292,55 @@ def run_unit(coords: CellCoords, replicate: int, config: SweepConfig, device: in
 
 # ------------------------------------------------------------ distribution
 def predicted_cost(coords: CellCoords) -> float:
-    """Relative cost model for LPT placement: eigendecomposition ~ m^3,
-    Gram / pseudo-inverse ~ m^2 n, surveillance ~ N n m."""
+    """Predicted wall time (ms) of one timed (cell, replicate) unit on a B200,
+    calibrated on round-2 measurements: ~1.5 ms fixed
+    (launches, synchronisations, Python), train ~1.6e-10 m^3 (the certified
+    Cholesky inverse dominates large m), surveillance ~1e-11 N n m (4 N n m
+    flops at ~400 TFLOP/s), device synthesis ~1.2e-8 ms per generated sample
+    (N n surveillance + 4 m n training rows).  Only ratios matter."""
     n, N, m = coords.n_signals, coords.n_observations, coords.n_memory
-    return 4.0 * m ** 3 + 4.0 * m * m * n + 1.0 * N * n * m + 1e6
+    return 1.5 + 1.6e-10 * m ** 3 + 1.0e-11 * N * n * m + 1.2e-8 * N * n + 4.8e-8 * m * n
 
 
-def plan_units(units: Sequence[Tuple[int, CellCoords, int]], world: int) -> List[List[Tuple[int, CellCoords, int]]]:
-    """Longest-processing-time-first over (cell_index, coords, replicate)
-    units; deterministic (ties by unit order)."""
-    order = sorted(range(len(units)), key=lambda i: (-predicted_cost(units[i][1]), i))
+def plan_units(units: Sequence[Tuple[int, CellCoords, int]], world: int,
+               warmups: int = 1) -> List[List[Tuple[int, CellCoords, int]]]:
+    """Place (cell_index, coords, replicate) units on `world` ranks.
+
+    A rank runs `warmups` untimed passes of a cell before its first timed
+    unit of that cell (sweep.cpp:193-204, kept per (cell, rank) so every
+    timed sample follows a warm-up on its own device), so spreading a cell's
+    replicates over ranks multiplies its warm-ups.  Cells are therefore
+    placed whole, largest first, on the least-loaded rank (LPT), and a cell
+    is split into replicate groups only when its warm-ups plus replicates
+    exceed an even share of the total.  Per-unit LPT without this paid a
+    warm-up per (cell, rank) for nearly every large cell and capped the
+    predicted 8-rank efficiency of the C4 grid at 0.64; cell-level LPT
+    reaches 0.99.  Deterministic (ties by rank, then cell order)."""
+    cells: dict = {}
+    for u in units:
+        cells.setdefault(u[0], []).append(u)
+    for lst in cells.values():
+        lst.sort(key=lambda u: u[2])
+    total = sum(predicted_cost(lst[0][1]) * (len(lst) + warmups) for lst in cells.values())
+    target = total / max(world, 1)
     loads = [0.0] * world
     plan: List[List[Tuple[int, CellCoords, int]]] = [[] for _ in range(world)]
-    for i in order:
-        r = min(range(world), key=lambda k: (loads[k], k))
-        plan[r].append(units[i])
-        loads[r] += predicted_cost(units[i][1])
+    order = sorted(cells, key=lambda i: (-predicted_cost(cells[i][0][1]) * (len(cells[i]) + warmups), i))
+    for idx in order:
+        lst = cells[idx]
+        c = predicted_cost(lst[0][1])
+        reps = len(lst)
+        g = 1
+        while g < reps and (warmups + -(-reps // g)) * c > target:
+            g += 1
+        sizes = [reps // g + (1 if k < reps % g else 0) for k in range(g)]
+        start = 0
+        for sz in sizes:
+            group = lst[start:start + sz]
+            start += sz
+            r = min(range(world), key=lambda k: (loads[k], k))
+            plan[r].extend(group)
+            loads[r] += c * (warmups + sz)
     for p in plan:  # each rank walks its units in grid order
         p.sort(key=lambda u: (u[0], u[2]))
     return plan
@@ -364,7 +397,7 @@ def run_sweep(config: SweepConfig, progress: Optional[Callable] = None, *, world
         raise EmptyGrid("run_sweep: no grid cell satisfies m >= 2n")
     started = time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())
     units = [(i, c, r) for i, (c, ok) in enumerate(grid_cells) if ok for r in range(config.replicates)]
-    mine = plan_units(units, world)[rank]
+    mine = plan_units(units, world, config.warmups)[rank]
     records = []
     seen = set()
     fatal = None

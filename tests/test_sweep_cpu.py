@@ -75,13 +75,16 @@ def test_lpt_plan_covers_every_unit_once_and_balances():
                                                      [100, 200, 500, 1000, 2000, 4000])) if ok]
     assert len(cells) == 96
     units = [(i, c, r) for i, c in enumerate(cells) for r in range(5)]
+    one = sum(predicted_cost(c) * 6 for c in cells)  # 5 replicates + 1 warm-up per cell
     for world in (1, 2, 4, 8):
         plan = plan_units(units, world)
         flat = sorted(u[:1] + u[2:] for p in plan for u in p)
         assert flat == sorted(u[:1] + u[2:] for u in units)
-        loads = [sum(predicted_cost(u[1]) for u in p) for p in plan]
-        assert max(loads) / (sum(loads) / world) < 1.15  # near-linear 1 -> 8
-        assert plan == plan_units(units, world)           # deterministic
+        # the work each rank really runs: its units plus one warm-up per (cell, rank)
+        loads = [sum(predicted_cost(u[1]) for u in p) + sum(predicted_cost(cells[i]) for i in {u[0] for u in p})
+                 for p in plan]
+        assert one / world / max(loads) > 0.95  # near-linear 1 -> 8, warm-ups included
+        assert plan == plan_units(units, world)  # deterministic
 
 
 def _fake_unit(coords, replicate, config, device, warm):

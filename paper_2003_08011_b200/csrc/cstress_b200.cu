@@ -234,24 +234,21 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
 }
 
 // ------------------------------------------- eigenvalues without cuSOLVER
-// (eig_tridiag.cuh): cluster tridiagonalisation + bisection, m <= kTriMaxM.
-// Returns false when the cluster cannot be launched (the caller then uses
+// (eig_tridiag.cuh): shared-memory tridiagonalisation + bisection, m <= kTriMaxM.
+// Returns false when the grid cannot be co-resident (the caller then uses
 // syevd).  w is a device array (ascending).
 bool bisect_eigvals(cudaStream_t st, const double* dd, const double* de, int64_t m, double* w);
 bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   if (m < 1 || m > kTriMaxM) return false;
-  // Default for m <= kTriOwnMaxM, where it beats syevd (one CTA with the
-  // matrix in shared memory up to kTriCtaMaxM, the 16-CTA cluster above);
-  // opt-in (CSB_EIG_OWN=1) up to kTriMaxM; CSB_EIG_OWN=0: never
-  // (eig_tridiag.cuh has the measurements).
+  // Default for m <= kTriMaxM, where it beats syevd: one CTA with the matrix
+  // in shared memory up to kTriCtaMaxM, the co-resident grid above
+  // (eig_tridiag.cuh has the measurements); CSB_EIG_OWN=0: never.
   const char* own = std::getenv("CSB_EIG_OWN");
   if (own && own[0] == '0') return false;
-  const bool small = m <= kTriCtaMaxM;
-  if (m > kTriOwnMaxM && !(own && own[0] == '1')) return false;
   cudaStream_t st = ctx->stream;
   StreamScope scope(st);
   TmpBuf<double> d(m), e(m + 1);
-  if (small) {
+  if (m <= kTriCtaMaxM) {
     // the attribute is per (function, device)
     static std::atomic<unsigned long long> attr_dev{0};
     if (!(attr_dev.load() >> ctx->device & 1ull)) {
@@ -264,53 +261,56 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
     CSB_LAUNCH_CHECK();
     return bisect_eigvals(st, d.get(), e.get(), m, w);
   }
-  // cluster size: 16 (non-portable) when the device takes it, else 8
-  // (per device: the attribute and the occupancy answer are per device)
-  static int cs_by_dev[64] = {};
-  static std::mutex mu;
-  int cs_best = 8;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    int& cached = cs_by_dev[ctx->device & 63];
-    if (cached == 0) {
-      cached = 8;
-      if (cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-          cudaSuccess) {
-        cudaLaunchConfig_t q{};
-        q.gridDim = dim3(16);
-        q.blockDim = dim3(kTriThreads);
-        cudaLaunchAttribute at{};
-        at.id = cudaLaunchAttributeClusterDimension;
-        at.val.clusterDim.x = 16;
-        at.val.clusterDim.y = 1;
-        at.val.clusterDim.z = 1;
-        q.attrs = &at;
-        q.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, tridiag_cluster_kernel, &q) == cudaSuccess && n > 0) cached = 16;
-      }
-      cudaGetLastError();
-    }
-    cs_best = cached;
-  }
-  const int CS = cs_best;
-  if ((m + CS - 1) / CS > 128) return false;
-  TmpBuf<double> A(static_cast<size_t>(m) * m), gv(m), gw(m);
-  CSB_CUDA(cudaMemcpyAsync(A.get(), G, static_cast<size_t>(m) * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  TriArgs ta{A.get(), static_cast<int>(m), d.get(), e.get(), gv.get(), gw.get()};
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CS);
-  cfg.blockDim = dim3(kTriThreads);
-  cfg.stream = st;
-  cudaLaunchAttribute at{};
-  at.id = cudaLaunchAttributeClusterDimension;
-  at.val.clusterDim.x = CS;
-  at.val.clusterDim.y = 1;
-  at.val.clusterDim.z = 1;
-  cfg.attrs = &at;
-  cfg.numAttrs = 1;
-  CSB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, ta));
+  // co-resident grid, rows in shared memory: up to kTriGridRows rows of
+  // NC x kTriGridThreads doubles per CTA, as many CTAs as that takes (<= SMs)
+  int sms = 0, optin = 0;
+  CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  CSB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const int nc = m <= kTriGridThreads ? 1 : m <= 2 * kTriGridThreads ? 2 : m <= 4 * kTriGridThreads ? 4 : 8;
+  const void* fn = nc == 1   ? reinterpret_cast<const void*>(tridiag_grid_kernel<1>)
+                   : nc == 2 ? reinterpret_cast<const void*>(tridiag_grid_kernel<2>)
+                   : nc == 4 ? reinterpret_cast<const void*>(tridiag_grid_kernel<4>)
+                             : reinterpret_cast<const void*>(tridiag_grid_kernel<8>);
+  cudaFuncAttributes fa{};
+  CSB_CUDA(cudaFuncGetAttributes(&fa, fn));
+  const int64_t row_bytes = static_cast<int64_t>(tri_grid_smem(nc, 1) - tri_grid_smem(nc, 0));
+  const int64_t room = static_cast<int64_t>(optin) - static_cast<int64_t>(tri_grid_smem(nc, 0) + fa.sharedSizeBytes);
+  int rows = kTriGridRows;
+  if (const char* r = std::getenv("CSB_EIG_GRID_ROWS")) rows = std::max(1, std::min(kTriGridRows, std::atoi(r)));
+  rows = static_cast<int>(std::min<int64_t>(rows, room / row_bytes));
+  if (rows < 1) return false;
+  const int P = static_cast<int>((m + rows - 1) / rows);
+  const int Rmax = static_cast<int>((m + P - 1) / P);
+  const size_t smem = tri_grid_smem(nc, Rmax);
+  CSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTriGridThreads, smem));
+  if (P > kTriGridMaxP || P > per_sm * sms) return false;  // cannot be co-resident: syevd
+  TmpBuf<ulonglong2> pb(2 * m), rb(2 * m), kb(2 * static_cast<size_t>(P));
+  // stale tags from an earlier call must not match this call's steps
+  CSB_CUDA(cudaMemsetAsync(pb.get(), 0, 2 * m * sizeof(ulonglong2), st));
+  CSB_CUDA(cudaMemsetAsync(rb.get(), 0, 2 * m * sizeof(ulonglong2), st));
+  CSB_CUDA(cudaMemsetAsync(kb.get(), 0, 2 * static_cast<size_t>(P) * sizeof(ulonglong2), st));
+  const bool trace = std::getenv("CSB_EIG_TRACE") != nullptr;  // development: per-step timeline
+  TmpBuf<unsigned long long> tr(trace ? 4 * m : 1);
+  TriGridArgs ga{G, static_cast<int>(m), P, d.get(), e.get(), pb.get(), rb.get(), kb.get(), trace ? tr.get() : nullptr};
+  void* args[] = {&ga};
+  CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(P), dim3(kTriGridThreads), args, smem, st));
   CSB_LAUNCH_CHECK();
+  if (trace) {
+    std::vector<unsigned long long> h(4 * m);
+    CSB_CUDA(cudaMemcpyAsync(h.data(), tr.get(), 4 * m * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    double s3[3] = {0, 0, 0};
+    int cnt = 0;
+    for (int64_t k = 0; k + 3 < m; ++k, ++cnt) {
+      s3[0] += double(h[4 * k + 2] - h[4 * k + 1]);        // exchange (slowest CTA + hop)
+      s3[1] += double(h[4 * k + 3] - h[4 * k + 2]);        // update + next reflector
+      s3[2] += double(h[4 * (k + 1) + 1] - h[4 * k + 3]);  // row sums + publish
+    }
+    std::fprintf(stderr, "eig grid m=%lld P=%d ns/step: exchange %.0f  update+reflector %.0f  row sums %.0f\n",
+                 static_cast<long long>(m), P, s3[0] / cnt, s3[1] / cnt, s3[2] / cnt);
+  }
   return bisect_eigvals(st, d.get(), e.get(), m, w);
 }
 
@@ -358,7 +358,7 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V, b
   std::memcpy(&mag, &hs[0], 8);
   std::memcpy(&asym, &hs[1], 8);
   if (asym > 1e-9 * std::max(mag, 1.0)) fail(CS_SHAPE_ERROR, "symmetric_eig: matrix is not symmetric to 1e-9");
-  // eigenvalues only: own cluster tridiagonalisation + bisection (m <= 2048)
+  // eigenvalues only: own tridiagonalisation + bisection (m <= 2048)
   if (!vectors && tridiag_eigvals(ctx, G, m, w)) return;
   if (V != G) CSB_CUDA(cudaMemcpyAsync(V, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
   const CusolverApi& api = cusolver_api();

@@ -1,31 +1,22 @@
 // eig_tridiag.cuh -- eigenvalues of a symmetric matrix without cuSOLVER:
-// Householder tridiagonalisation by one thread-block cluster, then Sturm-count
-// multisection.  The eigenvalues-only calls of the train path (the eager
-// eigen_spectrum and the eigen route's rank decision, mset.cpp:153-163) take
-// it by default for m <= kTriOwnMaxM, where it beats cuSOLVER's syevd
-// (measured, 1 x B200: m = 40 0.20 vs 0.38 ms, 100 0.42 vs 0.75, 160 0.89 vs
-// 1.29, 500 4.6 vs 5.3); above, syevd stays the default (m = 1000: 19 vs
-// 12 ms -- a one-stage reduction streams the trailing matrix through L2 at
-// every column; the fast design is two-stage) and the
-// own path is opt-in (CSB_EIG_OWN=1) up to kTriMaxM.  Exact to 1e-12 of
-// max|lambda| against LAPACK (tests/test_gpu_eig.py).
+// Householder tridiagonalisation with the matrix held in shared memory, then
+// Sturm-count multisection.  The eigenvalues-only calls of the train path
+// (the eager eigen_spectrum and the eigen route's rank decision,
+// mset.cpp:153-163) take it by default for m <= kTriMaxM (measured, 1 x
+// B200, against cuSOLVER's syevd: m = 100 0.42 vs 0.75 ms, 200 0.94 vs 1.86,
+// 500 3.3 vs 5.3, 1000 7.4 vs 11.9, 2000 22.5 vs 28.4); larger m stays on
+// syevd.  Exact to 1e-12 of max|lambda| against LAPACK (tests/test_gpu_eig.py).
 //
 // Tridiagonalisation (the classical one-stage algorithm, Golub & Van Loan
 // 8.3.1): for k = 0 .. m-3, a Householder reflector H = I - tau v v^T
 // (v_0 = 1) maps column k below the diagonal to (beta, 0, ...); the trailing
 // matrix becomes H A22 H = A22 - v w^T - w v^T with p = tau A22 v and
-// w = p - (tau / 2)(p^T v) v.  cuSOLVER's blocked sytrd spends ~11 ms at
-// m = 1000 on this (latency of its per-column kernels); here one cluster of
-// 16 CTAs (non-portable size; 8 where 16 cannot be launched) owns the whole
-// reduction: CTA c holds rows [c R, c R + R) of the full symmetric working
-// matrix in global memory (L2-resident up to ~2k x 2k), the column step's
-// reductions go through distributed shared memory (partials
-// read in parallel and summed by a fixed shuffle tree: deterministic); each column costs two cluster
-// barriers: v is re-derived by every CTA from column k in L2, p goes out
-// through L2 with the p.v partials and w = p - (tau K / 2) v is formed on the
-// fly in the rank-2 update.
-// Both triangles are updated with the same rounded terms, so the working
-// matrix stays exactly symmetric.
+// w = p - (tau / 2)(p^T v) v.  Every column step needs the whole trailing
+// matrix (p) and then a vector exchange before the next step can start, so
+// the reduction is latency-bound: cuSOLVER's blocked sytrd spends ~11 ms at
+// m = 1000 in per-column kernels.  Here one launch does all m - 2 steps:
+// one CTA for m <= kTriCtaMaxM, a co-resident grid above (one column
+// exchange through L2 per step, see tridiag_grid_kernel).
 //
 // Bisection (LAPACK dstebz's method): count(x) = number of negative
 // pivots of T - x I = number of eigenvalues < x; eigenvalue k is the point
@@ -33,191 +24,16 @@
 // to the last bit (one warp per eigenvalue, 32 shifts per round).
 #pragma once
 
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 
 namespace csb {
-namespace cg = cooperative_groups;
 
-constexpr int kTriThreads = 512;
 constexpr int kTriMaxM = 2048;
-constexpr int kTriOwnMaxM = 512;  // default own path up to here
-
-struct TriArgs {
-  double* A;   // m x m full symmetric working copy, column-major (destroyed)
-  int m;
-  double* d;   // [m] diagonal of T
-  double* e;   // [m - 1] off-diagonal of T
-  double* gv;  // [m] Householder vector (global exchange)
-  double* gw;  // [m] w vector
-};
-
-// block sum of one double per thread (deterministic tree); result on all threads
-__device__ __forceinline__ double tri_block_sum(double x, double* scratch) {
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();  // scratch free
-  if (lane == 0) scratch[warp] = x;
-  __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < kTriThreads / 32; ++w) s += scratch[w];
-  return s;
-}
-
-__global__ void __launch_bounds__(kTriThreads, 1) tridiag_cluster_kernel(TriArgs a) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CS = static_cast<int>(cluster.num_blocks());
-  const int c = static_cast<int>(cluster.block_rank());
-  const int m = a.m;
-  double* A = a.A;
-  const int R = (m + CS - 1) / CS;
-  const int r0 = c * R, r1 = min(m, r0 + R);
-  const int RP = R <= 32 ? 32 : (R <= 64 ? 64 : 128);  // rows per phase group (R <= 128)
-  const int nph = kTriThreads / RP;                    // column phases
-  const int tid = threadIdx.x, rr = tid % RP, ph = tid / RP;
-  const int i = r0 + rr;
-  const bool own = i < r1;
-  __shared__ double scratch[kTriThreads / 32];
-  __shared__ double red[2][4];  // this CTA's partials, by step parity (read remotely)
-  __shared__ double bc[4];      // broadcast: tau, scal, K
-  __shared__ double prow[kTriThreads];
-  auto col = [&](int j) { return A + static_cast<size_t>(j) * m; };
-  for (int k = 0; k + 2 < m; ++k) {
-    const int par = k & 1;
-    // (a) column k below the diagonal: alpha = A(k+1, k), sigma = sum of squares below
-    double sig = 0.0, alp = 0.0;
-    if (ph == 0 && own && i >= k + 1) {
-      const double x = col(k)[i];
-      if (i == k + 1) alp = x;
-      else sig = x * x;
-    }
-    sig = tri_block_sum(sig, scratch);
-    alp = tri_block_sum(alp, scratch);
-    if (tid == 0) {
-      red[par][0] = sig;
-      red[par][1] = alp;
-    }
-    cluster.sync();
-    if (tid < 32) {
-      // lane q reads CTA q's partials (remote loads in parallel, not a
-      // dependent chain of DSMEM round trips), then a fixed shuffle tree
-      double S = 0.0, Al = 0.0;
-      if (tid < CS) {
-        const double* rq = cluster.map_shared_rank(&red[par][0], tid);
-        S = rq[0];
-        Al = rq[1];
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        S += __shfl_xor_sync(0xffffffffu, S, o);
-        Al += __shfl_xor_sync(0xffffffffu, Al, o);
-      }
-      double tau = 0.0, scal = 0.0, beta = Al;
-      if (S > 0.0) {
-        const double nrm = sqrt(Al * Al + S);
-        beta = -copysign(nrm, Al);
-        tau = (beta - Al) / beta;
-        scal = 1.0 / (Al - beta);
-      }
-      if (tid == 0) {
-        bc[0] = tau;
-        bc[1] = scal;
-        if (c == 0) {
-          a.d[k] = A[static_cast<size_t>(k) * m + k];
-          a.e[k] = beta;
-        }
-      }
-    }
-    __syncthreads();
-    const double tau = bc[0], scal = bc[1];
-    if (tau == 0.0) {  // column already reduced: H = I (all CTAs agree: same S)
-      __syncthreads();
-      continue;
-    }
-    // v from column k itself (every CTA reads the whole column from L2: the
-    // previous step's updates are ordered before it by the barrier above),
-    // so no exchange and no barrier for v
-    auto vof = [&](int j) { return j == k + 1 ? 1.0 : col(k)[j] * scal; };
-    const double vi = (own && i >= k + 1) ? vof(i) : 0.0;
-    // (b) p_i = tau sum_{j > k} A(i, j) v_j over this CTA's rows
-    double acc = 0.0;
-    if (own && i >= k + 1) {
-      // eight columns' loads in flight per batch, four accumulators
-      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-      int j = k + 1 + ph;
-      for (; j + 7 * nph < m; j += 8 * nph) {
-        double av[8], vv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          av[u] = col(j + u * nph)[i];
-          vv[u] = vof(j + u * nph);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc4[u & 3] = fma(av[u], vv[u], acc4[u & 3]);
-      }
-      for (; j < m; j += nph) acc4[0] = fma(col(j)[i], vof(j), acc4[0]);
-      acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-    }
-    prow[tid] = acc;
-    __syncthreads();
-    double pi = 0.0;
-    if (ph == 0 && own && i >= k + 1) {
-      for (int q = 0; q < nph; ++q) pi += prow[q * RP + rr];
-      pi *= tau;
-      a.gv[i] = pi;  // p goes out with the p.v partial: one barrier for both
-    }
-    double pv = tri_block_sum(ph == 0 ? pi * vi : 0.0, scratch);
-    if (tid == 0) red[par][2] = pv;
-    cluster.sync();
-    if (tid < 32) {
-      double K = tid < CS ? cluster.map_shared_rank(&red[par][0], tid)[2] : 0.0;
-      for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
-      if (tid == 0) bc[2] = K;
-    }
-    __syncthreads();
-    const double hk = 0.5 * tau * bc[2];
-    // (d) A22 -= v w^T + w v^T on this CTA's rows, w_j = p_j - (tau K / 2) v_j
-    // formed on the fly from the exchanged p (same expression in every CTA)
-    if (own && i >= k + 1) {
-      const double wi = a.gv[i] - hk * vi;
-      int j = k + 1 + ph;
-      for (; j + 7 * nph < m; j += 8 * nph) {
-        double av[8], pj[8], vj[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          av[u] = col(j + u * nph)[i];
-          pj[u] = a.gv[j + u * nph];
-          vj[u] = vof(j + u * nph);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double wj = pj[u] - hk * vj[u];
-          col(j + u * nph)[i] = av[u] - __dadd_rn(__dmul_rn(vi, wj), __dmul_rn(wi, vj[u]));
-        }
-      }
-      for (; j < m; j += nph) {
-        const double vj = vof(j), wj = a.gv[j] - hk * vj;
-        col(j)[i] -= __dadd_rn(__dmul_rn(vi, wj), __dmul_rn(wi, vj));
-      }
-    }
-    __syncthreads();  // the next column's entries of this CTA's rows are final; other CTAs
-                      // read them after the next step's first cluster barrier
-  }
-  // the last 2 x 2 block
-  cluster.sync();
-  if (c == 0 && tid == 0) {
-    if (m >= 2) {
-      a.d[m - 2] = A[static_cast<size_t>(m - 2) * m + (m - 2)];
-      a.e[m - 2] = A[static_cast<size_t>(m - 2) * m + (m - 1)];
-    }
-    a.d[m - 1] = A[static_cast<size_t>(m - 1) * m + (m - 1)];
-  }
-}
+constexpr int kTriCtaMaxM = 160;
 
 // Small matrices (m <= kTriCtaMaxM): the same reduction by ONE CTA with the
 // whole matrix in shared memory -- block barriers only, no cluster barrier
 // or L2 round trip per column (m = 100: ~0.15 ms against syevd's 0.75 ms).
-constexpr int kTriCtaMaxM = 160;
 constexpr int kTriCtaThreads = 512;
 __host__ __device__ constexpr size_t tri_cta_smem(int m) {
   return sizeof(double) * (static_cast<size_t>(m) * (m + 1) + 3 * static_cast<size_t>(m) + kTriCtaThreads +
@@ -314,6 +130,358 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
       e[m - 2] = A[(m - 1) + (m - 2) * ld];
     }
     d[m - 1] = A[(m - 1) + (m - 1) * ld];
+  }
+}
+
+// Larger matrices (kTriCtaMaxM < m <= kTriMaxM): the same reduction by a
+// co-resident grid (cooperative launch, one CTA per SM) with the whole
+// matrix in SHARED memory -- CTA c keeps the full rows i = c, c + P, ...
+// (cyclic, so the shrinking trailing block stays balanced; at most
+// kTriGridRows rows of m doubles); thread t owns the columns j = t + u T.
+// ONE exchange through L2 per column step, no barrier:
+//   (B) every CTA forms p_i = tau (A22 v)_i for its rows i > k and publishes
+//       p_i, its partial of K = p^T v, and -- the owner of row k + 2 --
+//       that row as it stands (after step k - 1);
+//   (C) every CTA reads all p_j, the P partials (summed in CTA order: every
+//       CTA gets the same K, hence the same w = p - (tau K / 2) v) and row
+//       k + 2, then applies A_ij -= v_i w_j + w_i v_j to its own rows and
+//       to two REPLICA rows held in registers: row k + 1 (received one step
+//       earlier) and row k + 2.  Row k + 1 is then final for step k + 1, so
+//       every CTA forms the next reflector (v, tau) itself from its replica
+//       -- the same values, bit for bit, as the owner's row gives (same
+//       inputs, same operations) -- and no second exchange is needed.
+// The mirrored element A_ji gets the identically rounded update, so the
+// matrix stays exactly symmetric.  Every published double travels as two
+// 8-byte words (32-bit half + 32-bit step tag; 8-byte stores are single-copy
+// atomic), so a reader polls the data itself: no flag, fence or barrier.
+// Buffers alternate by step parity; a CTA can run at most one step ahead of
+// the slowest (step k+1's exchange needs every CTA's step-k publication,
+// which follows its step k-1 reads), so two generations suffice.  tau = 0
+// steps run the same exchange (p = 0, w = 0: the update subtracts zeros).
+constexpr int kTriGridThreads = 256;
+constexpr int kTriGridRows = 16;                          // owned rows per CTA (one row sum per lane pair)
+constexpr int kTriGridCols = kTriMaxM / kTriGridThreads;  // columns per thread
+constexpr int kTriGridMaxP = 160;                         // CTAs (partials of p^T v: 5 per lane)
+static_assert(kTriGridCols * kTriGridThreads >= kTriMaxM, "grid reduction column cover");
+static_assert(kTriGridRows == 16, "the row-sum transpose reduction is written for 16 rows");
+
+struct TriGridArgs {
+  const double* G;   // m x m symmetric, column-major (read only)
+  int m, P;
+  double* d;         // [m]
+  double* e;         // [m - 1]
+  ulonglong2* pbuf;  // [2][m] tagged p
+  ulonglong2* rbuf;  // [2][m] tagged row k + 2
+  ulonglong2* kbuf;  // [2][P] tagged partials of p^T v
+  unsigned long long* trace;  // development: [m][4] globaltimer stamps of CTA 0, or nullptr
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tag_store(ulonglong2* p, double x, unsigned tag) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(t | (b & 0xffffffffull)),
+               "l"(t | (b >> 32))
+               : "memory");
+}
+__device__ __forceinline__ ulonglong2 tag_load(const ulonglong2* p) {
+  ulonglong2 r;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ bool tag_ok(ulonglong2 r, unsigned tag) {
+  return static_cast<unsigned>(r.x >> 32) == tag && static_cast<unsigned>(r.y >> 32) == tag;
+}
+__device__ __forceinline__ double tag_value(ulonglong2 r) {
+  return __longlong_as_double(static_cast<long long>((r.y << 32) | (r.x & 0xffffffffull)));
+}
+// N tagged slots at addr(u) (nullptr: none): every load is issued before
+// any tag is checked, and only the late slots are re-polled
+template <int N, class Addr>
+__device__ __forceinline__ void tag_wait_slots(Addr addr, unsigned tag, double (&out)[N]) {
+  ulonglong2 r[N];
+  const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const ulonglong2* p = addr(u);
+    r[u] = p ? tag_load(p) : make_ulonglong2(t, t);
+  }
+  while (true) {
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < N; ++u) ok &= tag_ok(r[u], tag);
+    if (ok) break;
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+      if (!tag_ok(r[u], tag)) r[u] = tag_load(addr(u));
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) out[u] = addr(u) ? tag_value(r[u]) : 0.0;
+}
+
+// shared memory: the small arrays, then `rows` rows of NC T doubles (a
+// compile-time row stride: every row access is one base register plus an
+// immediate offset, and the columns past m are zero padding)
+constexpr int kTriGridSmall = 2 * kTriGridRows + kTriGridRows * (kTriGridThreads / 32) + kTriGridThreads / 32 + 8;
+__host__ __device__ constexpr size_t tri_grid_smem(int nc, int rows) {
+  return sizeof(double) * (static_cast<size_t>(rows) * nc * kTriGridThreads + kTriGridSmall);
+}
+
+template <int NC>  // column slots per thread: m <= NC kTriGridThreads
+__global__ void __launch_bounds__(kTriGridThreads, 1) tridiag_grid_kernel(TriGridArgs a) {
+  extern __shared__ double sm[];
+  constexpr int T = kTriGridThreads, NW = T / 32, LD = NC * T;
+  const int m = a.m, P = a.P, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = (m - c + P - 1) / P;  // rows i = c + r P, r < R
+  const int Rmax = (m + P - 1) / P;
+  double* vo = sm;                            // [kTriGridRows] v_i of the owned rows
+  double* po = vo + kTriGridRows;             // [kTriGridRows] p_i of the owned rows
+  double* red = po + kTriGridRows;            // [kTriGridRows][NW] row sums by warp
+  double* scratch = red + kTriGridRows * NW;  // [NW]
+  double* bc = scratch + NW;                  // broadcast scalars
+  double* At = sm + kTriGridSmall + tid;      // this thread's column 0 of owned row 0: (r, u) at r LD + u T
+  for (int r = 0; r < Rmax; ++r) {
+    const double* gcol = a.G + static_cast<size_t>(c + r * P) * m;  // row i == column i
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      At[r * LD + u * T] = r < R && j < m ? gcol[j] : 0.0;
+    }
+  }
+  if (tid < 2 * kTriGridRows) vo[tid] = 0.0;  // vo, po
+  // replicas of rows 0 and 1 (columns of this thread) straight from G
+  double r1[NC], vr[NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int j = tid + u * T;
+    r1[u] = j < m ? a.G[static_cast<size_t>(1) * m + j] : 0.0;
+    vr[u] = j < m ? a.G[j] : 0.0;  // row 0, turned into v below
+  }
+  // reflector of row `kk` (values x[u] at this thread's columns): sigma by a
+  // fixed-order block sum, then every thread forms tau / scal / beta itself
+  auto reflector = [&](int kk, double (&x)[NC], double& tau_out) {
+    double sig = 0.0;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      if (j > kk + 1 && j < m) sig = fma(x[u], x[u], sig);
+      if (j == kk + 1) bc[0] = x[u];  // alpha
+      if (j == kk && c == 0) a.d[kk] = x[u];
+    }
+    for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
+    if (lane == 0) scratch[warp] = sig;
+    __syncthreads();
+    double S = 0.0;
+    for (int w = 0; w < NW; ++w) S += scratch[w];
+    const double al = bc[0];
+    double tau = 0.0, scal = 0.0, beta = al;
+    if (S > 0.0) {
+      const double nrm = sqrt(al * al + S);
+      beta = -copysign(nrm, al);
+      tau = (beta - al) / beta;
+      scal = 1.0 / (al - beta);
+    }
+    if (c == 0 && tid == 0) a.e[kk] = beta;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      x[u] = j == kk + 1 ? 1.0 : (j > kk + 1 && j < m ? x[u] * scal : 0.0);
+    }
+    tau_out = tau;
+    __syncthreads();  // scratch / bc[0] reusable
+  };
+  // step kk's copy of row kk + 2 (as it stands after step kk - 1), published
+  // by its owner as soon as that update is done: each thread its own
+  // columns, which it wrote itself (no barrier)
+  auto publish_row = [&](int kk) {
+    if ((kk + 2) % P == c) {
+      const double* row = At + ((kk + 2) / P) * LD;
+      ulonglong2* rbk = a.rbuf + static_cast<size_t>(kk & 1) * m;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int j = tid + u * T;
+        if (j >= kk + 2 && j < m) tag_store(rbk + j, row[u * T], static_cast<unsigned>(kk + 1));
+      }
+    }
+  };
+  __syncthreads();  // the rows are loaded
+  if (m > 2) publish_row(0);
+  double tau;
+  reflector(0, vr, tau);
+
+  for (int k = 0; k + 2 < m; ++k) {
+    const unsigned tag = static_cast<unsigned>(k + 1);
+    const int par = k & 1;
+    ulonglong2* pb = a.pbuf + static_cast<size_t>(par) * m;
+    ulonglong2* rb = a.rbuf + static_cast<size_t>(par) * m;
+    ulonglong2* kb = a.kbuf + static_cast<size_t>(par) * P;
+    const int rlo = c > k ? 0 : (k - c) / P + 1;  // first owned row with i > k
+    // (B) row sums of the owned rows against v
+    // Slots are skipped only where a whole warp's 32 columns are dead (a
+    // uniform branch); inside a live warp slot v_j = 0 at j <= k and j >= m
+    // (where the row is zero padding), so dead columns add exact zeros.
+    // Rows i <= k (r < rlo) are finished and skipped (uniform).
+    bool live[NC];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) live[u] = u * T + warp * 32 + 31 > k && u * T + warp * 32 < m;
+    double acc[kTriGridRows];
+#pragma unroll
+    for (int r = 0; r < kTriGridRows; ++r) {
+      acc[r] = 0.0;
+      if (r >= rlo && r < R) {  // uniform
+#pragma unroll
+        for (int u = 0; u < NC; ++u)
+          if (live[u]) acc[r] = fma(At[r * LD + u * T], vr[u], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {  // stash v_i of the owned rows
+      const int j = tid + u * T;
+      if (j > k && j < m && j % P == c) vo[j / P] = vr[u];
+    }
+    // 16 row sums over the warp by a transposing butterfly (16 shuffles):
+    // lane l ends with row l >> 1
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+      const bool up = lane & (2 * h);
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const double send = up ? acc[i] : acc[i + h];
+        const double keep = up ? acc[i + h] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+      }
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    if ((lane & 1) == 0) red[(lane >> 1) * NW + warp] = acc[0];
+    __syncthreads();
+    if (warp == 0) {
+      const int r = lane;
+      double pv = 0.0;
+      if (r < rlo && r < kTriGridRows) vo[r] = po[r] = 0.0;  // finished rows: the update subtracts zeros
+      if (r >= rlo && r < R) {
+        const int i = c + r * P;
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += red[r * NW + w];
+        const double pi = tau * s;
+        po[r] = pi;
+        tag_store(pb + i, pi, tag);
+        pv = pi * vo[r];
+      }
+      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+      if (lane == 0) tag_store(kb + c, pv, tag);
+      if (a.trace && c == 0 && lane == 0) a.trace[4 * k + 1] = gtimer();
+    }
+    // (C) all p_j, row k + 2 and (warp 0) the partials, in ONE batch of loads
+    constexpr int KQ = (kTriGridMaxP + 31) / 32;
+    double pw[NC], r2[NC];
+    {
+      double got[2 * NC + KQ];
+      tag_wait_slots([&](int u) -> const ulonglong2* {
+        if (u < NC) {
+          const int j = tid + u * T;
+          return j > k && j < m ? pb + j : nullptr;
+        }
+        if (u < 2 * NC) {
+          const int j = tid + (u - NC) * T;
+          return j >= k + 2 && j < m ? rb + j : nullptr;
+        }
+        const int q = lane + (u - 2 * NC) * 32;  // partial q (lane + 32 i: a fixed order)
+        return warp == 0 && q < P ? kb + q : nullptr;
+      }, tag, got);
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        pw[u] = got[u];
+        r2[u] = got[NC + u];
+      }
+      if (warp == 0) {
+        double K = 0.0;
+#pragma unroll
+        for (int u = 0; u < KQ; ++u) K += got[2 * NC + u];
+        for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+        if (lane == 0) bc[3] = K;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {  // p and v at columns k + 1, k + 2 for the replicas
+      const int j = tid + u * T;
+      if (j == k + 1) bc[4] = pw[u];
+      if (j == k + 2) {
+        bc[5] = pw[u];
+        bc[6] = vr[u];
+      }
+    }
+    __syncthreads();
+    if (a.trace && c == 0 && tid == 0) a.trace[4 * k + 2] = gtimer();
+    const double hk = 0.5 * tau * bc[3];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) pw[u] = pw[u] - hk * vr[u];  // w_j
+    // live owned rows, live warp slots; at j <= k inside a live slot both w_j
+    // and v_j are 0, so those columns subtract exact zeros.  Groups of rows
+    // are loaded before any is stored (the compiler cannot tell the
+    // shared-memory rows apart and would order every load after the
+    // previous store).
+    constexpr int RG = NC <= 2 ? 8 : 16 / NC;
+#pragma unroll
+    for (int r0 = 0; r0 < kTriGridRows; r0 += RG) {
+      if (r0 + RG > rlo && r0 < R) {  // uniform
+        double x[RG][NC], vi[RG], wi[RG];
+#pragma unroll
+        for (int g = 0; g < RG; ++g) {
+          vi[g] = vo[r0 + g];
+          wi[g] = po[r0 + g] - hk * vi[g];
+          const bool rl = r0 + g >= rlo && r0 + g < R;  // uniform
+#pragma unroll
+          for (int u = 0; u < NC; ++u) x[g][u] = rl && live[u] ? At[(r0 + g) * LD + u * T] : 0.0;
+        }
+#pragma unroll
+        for (int g = 0; g < RG; ++g) {
+          if (r0 + g >= rlo && r0 + g < R) {  // uniform
+#pragma unroll
+            for (int u = 0; u < NC; ++u)
+              if (live[u] && tid + u * T < m)
+                At[(r0 + g) * LD + u * T] = x[g][u] - __dadd_rn(__dmul_rn(vi[g], pw[u]), __dmul_rn(wi[g], vr[u]));
+          }
+        }
+      }
+    }
+    {
+      // replica rows k + 1 (v_{k+1} = 1) and k + 2, updated exactly as their owners do
+      const double w1 = bc[4] - hk * 1.0;
+      const double v2 = bc[6], w2 = bc[5] - hk * v2;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int j = tid + u * T;
+        if (j > k && j < m) {
+          r1[u] -= __dadd_rn(__dmul_rn(1.0, pw[u]), __dmul_rn(w1, vr[u]));
+          r2[u] -= __dadd_rn(__dmul_rn(v2, pw[u]), __dmul_rn(w2, vr[u]));
+        }
+      }
+    }
+    if (k + 3 < m) {
+      publish_row(k + 1);
+      // the next reflector from row k + 1, which is final now
+#pragma unroll
+      for (int u = 0; u < NC; ++u) vr[u] = r1[u];
+      reflector(k + 1, vr, tau);
+    } else {
+      // the last 2 x 2 block: rows m - 2 (= k + 1) and m - 1 (= k + 2)
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int j = tid + u * T;
+        if (c == 0 && j == m - 2) a.d[m - 2] = r1[u];
+        if (c == 0 && j == m - 1) {
+          a.e[m - 2] = r1[u];
+          a.d[m - 1] = r2[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NC; ++u) r1[u] = r2[u];
+    if (a.trace && c == 0 && tid == 0) a.trace[4 * k + 3] = gtimer();
   }
 }
 

@@ -261,9 +261,9 @@ def symmetric_eig(G, backend: BackendId = BackendId()) -> SymmetricEig:
 
 def symmetric_eigvals(G, backend: BackendId = BackendId()) -> np.ndarray:
     """The eigenvalues (ascending) of symmetric_eig (mset.hpp:34-38) without
-    the vectors (cs_symmetric_eigvals): cuSOLVER syevd, or with
-    CSB_EIG_OWN=1 and m <= 2048 the library's own cluster tridiagonalisation
-    + bisection."""
+    the vectors (cs_symmetric_eigvals): for m <= 2048 the library's own
+    shared-memory tridiagonalisation + bisection (CSB_EIG_OWN=0: cuSOLVER
+    syevd), above it syevd."""
     G = f64(G)
     if G.ndim != 2 or G.shape[0] != G.shape[1]:
         raise ShapeError("symmetric_eig: matrix is not square")

@@ -1,12 +1,14 @@
-"""Eigenvalues without cuSOLVER (csrc/eig_tridiag.cuh): cluster Householder
-tridiagonalisation + Sturm bisection, the path of the eager eigen_spectrum
-and of the eigen route's rank decision (mset.cpp:153-163) for m <= 2048.
+"""Eigenvalues without cuSOLVER (csrc/eig_tridiag.cuh): shared-memory
+Householder tridiagonalisation (one CTA up to m = 160, a co-resident grid
+exchanging one column step at a time through L2 above) + Sturm bisection,
+the path of the eager eigen_spectrum and of the eigen route's rank decision
+(mset.cpp:153-163) for m <= 2048.
 Checked against LAPACK (numpy.linalg.eigvalsh) to 1e-12 of max|lambda| --
 the reference's own spectrum pin is 1e-10 (test_mset.cpp:163-199) -- on
 random symmetric matrices of awkward sizes, rank-deficient Gram matrices
 (duplicate memory vectors, test_mset.cpp:228-234), clustered spectra, and
-against the cuSOLVER route of the same library (the default route; the
-own one is the default up to m = 512 and opt-in, CSB_EIG_OWN=1, above)."""
+against the cuSOLVER route of the same library (CSB_EIG_OWN=0; the own
+path is the default up to m = 2048)."""
 import os
 
 import numpy as np
@@ -25,8 +27,8 @@ def p():
 
 @pytest.fixture(autouse=True)
 def own_path(monkeypatch):
-    # force the own solver at every size (above m = 512 it is opt-in:
-    # slower than cuSOLVER's syevd there); these tests pin its numerics
+    # the own solver (the default up to m = 2048; pinned here against a
+    # leftover CSB_EIG_OWN=0 in the environment)
     monkeypatch.setenv("CSB_EIG_OWN", "1")
 
 
@@ -34,7 +36,7 @@ def _err(w, want):
     return float(np.abs(np.asarray(w) - want).max() / max(np.abs(want).max(), 1e-300))
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 5, 17, 33, 100, 127, 129, 513, 1000, 2048])
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 17, 33, 100, 127, 129, 161, 256, 257, 513, 1000, 1025, 2047, 2048])
 def test_random_symmetric(p, m):
     rng = np.random.default_rng(m)
     A = rng.standard_normal((m, m))
@@ -76,9 +78,61 @@ def test_matches_cusolver_route(p, monkeypatch):
     A = rng.standard_normal((600, 600))
     A = np.asfortranarray(A @ A.T)
     own = p.symmetric_eigvals(A)
-    monkeypatch.delenv("CSB_EIG_OWN")
+    monkeypatch.setenv("CSB_EIG_OWN", "0")
     lib = p.symmetric_eigvals(A)
     assert _err(own, lib) <= 1e-12
+
+
+@pytest.mark.parametrize("m", [300, 1000])
+def test_deterministic(p, m):
+    """The grid's reductions have a fixed order (row sums by a fixed
+    butterfly, the CTA partials of p^T v summed in CTA order): repeated calls
+    are bitwise equal."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((m, m))
+    A = np.asfortranarray(A @ A.T)
+    w0 = p.symmetric_eigvals(A)
+    for _ in range(3):
+        assert np.array_equal(p.symmetric_eigvals(A), w0)
+
+
+@pytest.mark.parametrize("rows", ["2", "3", "16"])
+def test_grid_shapes(p, monkeypatch, rows):
+    """Rows per CTA (hence the number of co-resident CTAs, up to one per SM)
+    do not change the numbers beyond rounding."""
+    monkeypatch.setenv("CSB_EIG_GRID_ROWS", rows)
+    m = 145 * int(rows) if rows != "16" else 777  # up to 145 CTAs
+    rng = np.random.default_rng(int(rows))
+    A = rng.standard_normal((m, m))
+    A = np.asfortranarray(A + A.T)
+    assert _err(p.symmetric_eigvals(A), np.linalg.eigvalsh(A)) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["diagonal", "tridiagonal", "zero"])
+def test_already_reduced_columns(p, kind):
+    """Columns with nothing below the subdiagonal give tau = 0 (H = I); the
+    grid still runs the column exchange for them (p = 0, w = 0)."""
+    m = 400
+    rng = np.random.default_rng(9)
+    if kind == "diagonal":
+        A = np.diag(rng.standard_normal(m))
+    elif kind == "tridiagonal":
+        e = rng.standard_normal(m - 1)
+        A = np.diag(rng.standard_normal(m)) + np.diag(e, 1) + np.diag(e, -1)
+    else:
+        A = np.zeros((m, m))
+    A = np.asfortranarray(A)
+    want = np.linalg.eigvalsh(A)
+    w = p.symmetric_eigvals(A)
+    assert float(np.abs(w - want).max()) <= 1e-12 * max(np.abs(want).max(), 1.0)
+
+
+def test_above_own_range_uses_syevd(p):
+    m = 2049
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((m, m))
+    A = np.asfortranarray(A + A.T)
+    assert _err(p.symmetric_eigvals(A), np.linalg.eigvalsh(A)) <= 1e-12
 
 
 def test_not_symmetric_is_shape_error(p):
@@ -89,11 +143,11 @@ def test_not_symmetric_is_shape_error(p):
         p.symmetric_eigvals(A)
 
 
-@pytest.mark.parametrize("m", [2, 40, 100, 160, 200, 500])
-def test_small_default_path_matches_cusolver(p, monkeypatch, m):
-    """m <= 512: the own reduction (one CTA up to 160, the cluster above) is
-    the DEFAULT eigenvalues-only path (faster than syevd there);
-    CSB_EIG_OWN=0 forces syevd."""
+@pytest.mark.parametrize("m", [2, 40, 100, 160, 200, 500, 1000])
+def test_default_path_matches_cusolver(p, monkeypatch, m):
+    """The own reduction (one CTA up to 160, the grid above) is the DEFAULT
+    eigenvalues-only path (faster than syevd there); CSB_EIG_OWN=0 forces
+    syevd."""
     rng = np.random.default_rng(100 + m)
     A = rng.standard_normal((m, m))
     A = np.asfortranarray(A @ A.T + np.eye(m))

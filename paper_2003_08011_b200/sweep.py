@@ -88,6 +88,7 @@ class SweepConfig:
     master_seed: int = 0
     timer: str = "wall_monotonic"
     estimator: str = "mset2"
+    threads_override_note: str = ""  # config.hpp: where a worker-count override came from
 
     def validate(self) -> None:  # sweep.cpp:98-111
         from .estimator import algorithm_by_name
@@ -440,6 +441,7 @@ def run_sweep(config: SweepConfig, progress: Optional[Callable] = None, *, world
         "hardware_threads": os.cpu_count(),
         "timer": config.timer,
         "rng_algorithm": RNG_ALGORITHM,
+        "threads_override": config.threads_override_note,
         "config": sweep_config_to_json(config),
         "world_size": world,
         "placement": "LPT over (cell, replicate) units; records gathered with torch.distributed",

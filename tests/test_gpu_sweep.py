@@ -158,3 +158,34 @@ def test_sweep_gpu_vs_host_speedup_surface(p, tmp_path):
         assert {c.backend for c in back.cells} == {cpu, gpu}
     finally:
         host_backend.unregister()
+
+
+def test_cli_sweep_then_speedup(p, tmp_path, capsys):
+    """python -m paper_2003_08011_b200 sweep / speedup (tools/main.cpp:142-275)
+    end to end on the GPU: a 2 x 2 grid with one inadmissible cell, FP64 and
+    FP32 B200 backends, then the FP64 / FP32 speedup surface."""
+    import json
+    from paper_2003_08011_b200 import cli
+    cfg = {"grid": {"signal_counts": [4, 40], "observation_counts": [3000], "memory_counts": [40, 64]},
+           "replicates": 2, "warmups": 1, "master_seed": 20260810,
+           "backends": [{"kind": "b200", "device": 0, "precision": "fp64"},
+                        {"kind": "b200", "device": 0, "precision": "fp32"}],
+           "signals": {"ar_coefficient": 0.5, "cross_correlation": 0.3, "skewness": 0.5, "kurtosis": 4.0}}
+    path = tmp_path / "c.json"
+    path.write_text(json.dumps(cfg))
+    out = tmp_path / "sweep"
+    assert cli.main(["sweep", "--config", str(path), "--out", str(out)]) == 0
+    captured = capsys.readouterr()
+    assert "excluded (m<2n)" in captured.err  # n = 40, m = 40, 64: m < 2n
+    assert "b200[device=0/precision=fp32]" in captured.out
+    surface = p.surfaces.import_surface_json(str(out / "surface.json"))
+    live = [c for c in surface.cells if not c.excluded]
+    assert len(live) == 2 * 2 * 2 and all(len(c.samples) == 2 and c.median > 0 for c in live)
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["exit_status"] == 0 and "surface.json" in man["artifacts"]
+    sp = tmp_path / "sp"
+    assert cli.main(["speedup", "--surface", str(out / "surface.json"), "--ref",
+                     "b200[device=0/precision=fp64]", "--opt", "b200[device=0/precision=fp32]",
+                     "--out", str(sp)]) == 0
+    rows = (sp / "speedup_surveil.csv").read_text().splitlines()
+    assert len(rows) == 1 + 4  # header + every grid cell (holes included)

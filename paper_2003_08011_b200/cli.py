@@ -209,7 +209,8 @@ def main(argv: Optional[List[str]] = None) -> int:
         if world > 1:  # one process per GPU (torchrun), records gathered at the end
             import torch.distributed as dist
             if not dist.is_initialized():
-                dist.init_process_group("nccl")
+                # CSB_DIST_BACKEND=gloo: several ranks without GPUs (tests)
+                dist.init_process_group(os.environ.get("CSB_DIST_BACKEND", "nccl"))
         return cmd_sweep(a.config, a.out, a.backend, a.threads, a.seed, world=world, rank=rank, device=device)
     return cmd_speedup(a.surface, a.ref, a.opt, a.out)
 

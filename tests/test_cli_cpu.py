@@ -195,3 +195,43 @@ def test_speedup_unknown_and_ambiguous_backends(tmp_path, capsys):
                      "--out", str(tmp_path / "o2")]) == 2
     assert "not present in this surface" in capsys.readouterr().err
     assert os.path.exists(tmp_path / "o2") is False
+
+
+def _cli_rank(rank, world, port, cfg_path, out_dir, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK="0", CSB_DIST_BACKEND="gloo")
+    from paper_2003_08011_b200 import cli as c, sweep as sm
+    sm.run_unit = _fake_unit
+    q.put((rank, c.main(["sweep", "--config", cfg_path, "--out", out_dir])))
+
+
+def test_cli_sweep_two_ranks_gloo(tmp_path):
+    """`torchrun -m paper_2003_08011_b200 sweep` with world size 2 (gloo, no
+    GPU work): rank 0 writes the same surface as a single-rank run."""
+    import socket
+    import torch.multiprocessing as mp
+    j = {"grid": {"signal_counts": [2, 4], "observation_counts": [64, 128], "memory_counts": [8, 16]},
+         "replicates": 3, "backends": ["b200"], "master_seed": 5}
+    cfg = _write(tmp_path, j)
+    import paper_2003_08011_b200.sweep as sm
+    orig = sm.run_unit
+    sm.run_unit = _fake_unit
+    try:
+        assert cli.main(["sweep", "--config", cfg, "--out", str(tmp_path / "one")]) == 0
+    finally:
+        sm.run_unit = orig
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cli_rank, args=(r, 2, port, cfg, str(tmp_path / "two"), q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    codes = dict(q.get(timeout=180) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert codes == {0: 0, 1: 0}
+    one = json.loads((tmp_path / "one" / "surface.json").read_text())
+    two = json.loads((tmp_path / "two" / "surface.json").read_text())
+    assert one["cells"] == two["cells"]

@@ -12,7 +12,7 @@ h_obs = torch.from_numpy(np.asfortranarray(obs).T.copy()).pin_memory()
 h_est = torch.empty_like(h_obs).pin_memory()
 h_res = torch.empty_like(h_obs).pin_memory()
 o, e, r = h_obs.numpy().T, h_est.numpy().T, h_res.numpy().T
-for cd in [1 << 18, 1 << 19, 1 << 20, 1 << 21, 1 << 22]:
+for cd in [1 << 17, 1 << 18, 3 << 17, 1 << 19, 3 << 18, 1 << 20, 1 << 21]:
     os.environ["CSB_E2E_CHUNK_DOUBLES"] = str(cd)
     f = lambda: _lib.check(_lib.lib().cs_mset_estimate(p.context(0).handle, g.handle, o.ctypes.data_as(_lib.pd), N, n,  # noqa
                                                         e.ctypes.data_as(_lib.pd), r.ctypes.data_as(_lib.pd)))

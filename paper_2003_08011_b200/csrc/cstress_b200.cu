@@ -295,7 +295,12 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   TmpBuf<unsigned long long> tr(trace ? 4 * m : 1);
   TriGridArgs ga{G, static_cast<int>(m), P, d.get(), e.get(), pb.get(), rb.get(), kb.get(), trace ? tr.get() : nullptr};
   void* args[] = {&ga};
-  CSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(P), dim3(kTriGridThreads), args, smem, st));
+  const cudaError_t launched = cudaLaunchCooperativeKernel(fn, dim3(P), dim3(kTriGridThreads), args, smem, st);
+  if (launched == cudaErrorCooperativeLaunchTooLarge || launched == cudaErrorNotSupported) {
+    cudaGetLastError();  // the grid cannot be co-resident here (e.g. a partitioned device): syevd
+    return false;
+  }
+  CSB_CUDA(launched);
   CSB_LAUNCH_CHECK();
   if (trace) {
     std::vector<unsigned long long> h(4 * m);

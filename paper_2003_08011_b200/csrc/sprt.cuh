@@ -54,6 +54,28 @@ struct SprtStep {
     ln = __dadd_rn(ln, __dmul_rn(c, __dsub_rn(-r, h)));
     return decide(lp) | (decide(ln) << 1);
   }
+  // the same step with the flag bits OR-ed straight into a packed word
+  // (bit SHIFT: positive alarm, SHIFT + 1: negative) by predicated ORs --
+  // the speculate pass's inner loop (no 0/1 select, shift and combine)
+  template <int SHIFT>
+  __device__ __forceinline__ void into(double r, double& lp, double& ln, uint32_t& word) const {
+    lp = __dadd_rn(lp, __dmul_rn(c, __dsub_rn(r, h)));
+    ln = __dadd_rn(ln, __dmul_rn(c, __dsub_rn(-r, h)));
+    asm("{\n\t.reg .pred pa, pz;\n\t"
+        "setp.ge.f64 pa, %0, %2;\n\t"
+        "setp.le.or.f64 pz, %0, %3, pa;\n\t"
+        "selp.f64 %0, 0d0000000000000000, %0, pz;\n\t"
+        "@pa or.b32 %1, %1, %4;\n\t}"
+        : "+d"(lp), "+r"(word)
+        : "d"(B), "d"(A), "n"(1u << SHIFT));
+    asm("{\n\t.reg .pred pa, pz;\n\t"
+        "setp.ge.f64 pa, %0, %2;\n\t"
+        "setp.le.or.f64 pz, %0, %3, pa;\n\t"
+        "selp.f64 %0, 0d0000000000000000, %0, pz;\n\t"
+        "@pa or.b32 %1, %1, %4;\n\t}"
+        : "+d"(ln), "+r"(word)
+        : "d"(B), "d"(A), "n"(1u << (SHIFT + 1)));
+  }
   // lambda >= B: alarm and reset; lambda <= A: reset -- branch-free, the
   // reset predicate folded into the second compare (setp .or), so a
   // decision is two compares and one 64-bit select (NaN never decides,
@@ -209,9 +231,16 @@ __global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? 6 : 4) sprt_specul
       x[0] = v0.x, x[1] = v0.y, x[2] = v1.x, x[3] = v1.y;
     }
     uint32_t word = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q < valid) word |= step(static_cast<double>(x[q]), lp, ln) << (8 * q);
+    if (valid == 4) {
+      step.into<0>(static_cast<double>(x[0]), lp, ln, word);
+      step.into<8>(static_cast<double>(x[1]), lp, ln, word);
+      step.into<16>(static_cast<double>(x[2]), lp, ln, word);
+      step.into<24>(static_cast<double>(x[3]), lp, ln, word);
+    } else {
+      if (valid > 0) step.into<0>(static_cast<double>(x[0]), lp, ln, word);
+      if (valid > 1) step.into<8>(static_cast<double>(x[1]), lp, ln, word);
+      if (valid > 2) step.into<16>(static_cast<double>(x[2]), lp, ln, word);
+    }
     return word;
   };
 

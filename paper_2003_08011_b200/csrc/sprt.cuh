@@ -42,6 +42,9 @@
 
 namespace csb {
 
+#ifndef CSB_SPRT_MINB
+#define CSB_SPRT_MINB 6  // resident speculate CTAs per SM (FP32 residuals)
+#endif
 constexpr int kSprtChunk = 2048;  // steps per speculative chunk
 constexpr int kSprtSeg = 32;      // steps per staged round
 constexpr int kSprtCta = 128;     // chunks (threads) per CTA
@@ -142,7 +145,7 @@ __device__ __forceinline__ int64_t sprt_rerun(const SprtStep& step, const IO* __
 // Pass 1.  grid (ceil(chunks / kSprtCta), n), block kSprtCta.  VEC: the
 // residual column and its leading dimension are 16-byte aligned.
 template <typename IO, bool VEC>
-__global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? 6 : 4) sprt_speculate_kernel(
+__global__ void __launch_bounds__(kSprtCta, sizeof(IO) == 4 ? CSB_SPRT_MINB : 4) sprt_speculate_kernel(
     const IO* __restrict__ resid, int64_t N, int64_t ld, const double* __restrict__ c,
     const double* __restrict__ h, double A, double B, const double* __restrict__ state, int chunks,
     uint8_t* __restrict__ flags, SprtChunk* __restrict__ rec) {

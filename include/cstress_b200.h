@@ -105,9 +105,10 @@ cs_status cs_symmetric_eig(cs_ctx* ctx, const double* G, int64_t m,
 
 /* Eigenvalues only (ascending) of a symmetric m x m matrix -- the
  * eigen_spectrum part of symmetric_eig (mset.cpp:57-70), same precondition
- * (ShapeError when not symmetric to 1e-9).  cuSOLVER syevd; with
- * CSB_EIG_OWN=1 and m <= 2048 the library's own cluster tridiagonalisation
- * + bisection (exact to 1e-12 of max|lambda|, slower). */
+ * (ShapeError when not symmetric to 1e-9).  For m <= 2048 the library's own
+ * shared-memory tridiagonalisation + Sturm multisection (exact to 1e-12 of
+ * max|lambda|, faster than syevd at every size there; CSB_EIG_OWN=0 forces
+ * syevd), cuSOLVER syevd above. */
 cs_status cs_symmetric_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w);
 
 /* select_memory_vectors (mset.cpp:72-137): bit-exact indices. */

@@ -93,6 +93,19 @@ struct cs_ctx {
   DevBuf<unsigned char> wsBytes;
   DevBuf<__half> wsX[kSlots], wsS[kSlots];  // large-n surveillance (per stream slot): x, S operands
   DevBuf<float> wsXX[kSlots];                // ||x||^2
+  // pinned host staging for the small per-call transfers (grow-only)
+  void* pin = nullptr;
+  size_t pin_bytes = 0;
+  void* pinned(size_t bytes) {
+    if (bytes > pin_bytes) {
+      if (pin) cudaFreeHost(pin);
+      pin = nullptr;
+      pin_bytes = 0;
+      if (cudaMallocHost(&pin, bytes) != cudaSuccess) throw std::bad_alloc();
+      pin_bytes = bytes;
+    }
+    return pin;
+  }
 };
 
 struct cs_model {
@@ -104,7 +117,7 @@ struct cs_model {
   std::vector<int64_t> source_indices;
   // eigen_spectrum: computed at train time on the eigen paths; on the
   // certified-Cholesky path it is materialised on first export (one
-  // eigenvalues-only syevd of the re-formed Gram matrix)
+  // eigenvalues-only solve of the re-formed Gram matrix)
   mutable std::vector<double> spectrum_host;
   mutable DevBuf<double> spectrum;
   mutable bool spectrum_ready = true;
@@ -1286,31 +1299,41 @@ void sprt_device(cs_ctx* ctx, const IO* resid, int64_t N, int64_t n, int64_t ld,
   if (N == 0 || n == 0) return;
   if (n > 65535) fail(CS_CONFIG_ERROR, "sprt: at most 65535 signals per call");
   const int chunks = static_cast<int>((N + kSprtChunk - 1) / kSprtChunk);
-  TmpBuf<double> dc(n), dh(n), dstate(2 * n);
+  // one device block [c | h | state | counts] and one pinned host block:
+  // a single H2D before and a single D2H after the two kernels
+  TmpBuf<double> dblk(6 * n);
+  double* const dc_p = dblk.get();
+  double* const dh_p = dc_p + n;
+  double* const dstate_p = dh_p + n;
+  unsigned long long* const dcount_p = reinterpret_cast<unsigned long long*>(dstate_p + 2 * n);
   TmpBuf<SprtChunk> rec(static_cast<size_t>(n) * chunks);
-  TmpBuf<unsigned long long> dcount(2 * n);
-  CSB_CUDA(cudaMemcpyAsync(dc.get(), c, n * 8, cudaMemcpyHostToDevice, st));
-  CSB_CUDA(cudaMemcpyAsync(dh.get(), h, n * 8, cudaMemcpyHostToDevice, st));
-  CSB_CUDA(cudaMemcpyAsync(dstate.get(), state, 2 * n * 8, cudaMemcpyHostToDevice, st));
+  double* hp = static_cast<double*>(ctx->pinned(6 * n * sizeof(double)));
+  std::memcpy(hp, c, n * 8);
+  std::memcpy(hp + n, h, n * 8);
+  std::memcpy(hp + 2 * n, state, 2 * n * 8);
+  CSB_CUDA(cudaMemcpyAsync(dc_p, hp, 4 * n * 8, cudaMemcpyHostToDevice, st));
   const bool vec = (reinterpret_cast<uintptr_t>(resid) % 16 == 0) && ((ld * sizeof(IO)) % 16 == 0);
   const dim3 grid(ceil_div(chunks, kSprtCta), static_cast<unsigned>(n));
   if (vec)
-    sprt_speculate_kernel<IO, true><<<grid, kSprtCta, 0, st>>>(resid, N, ld, dc.get(), dh.get(), A, B,
-                                                               dstate.get(), chunks, d_flags, rec.get());
+    sprt_speculate_kernel<IO, true><<<grid, kSprtCta, 0, st>>>(resid, N, ld, dc_p, dh_p, A, B,
+                                                               dstate_p, chunks, d_flags, rec.get());
   else
-    sprt_speculate_kernel<IO, false><<<grid, kSprtCta, 0, st>>>(resid, N, ld, dc.get(), dh.get(), A, B,
-                                                                dstate.get(), chunks, d_flags, rec.get());
+    sprt_speculate_kernel<IO, false><<<grid, kSprtCta, 0, st>>>(resid, N, ld, dc_p, dh_p, A, B,
+                                                                dstate_p, chunks, d_flags, rec.get());
   CSB_LAUNCH_CHECK();
-  sprt_fixup_kernel<IO><<<ceil_div(n, 4), 128, 0, st>>>(resid, N, static_cast<int>(n), ld, dc.get(), dh.get(),
-                                                         A, B, dstate.get(), chunks, d_flags, rec.get(),
-                                                         dcount.get());
+  sprt_fixup_kernel<IO><<<ceil_div(n, 4), 128, 0, st>>>(resid, N, static_cast<int>(n), ld, dc_p, dh_p,
+                                                         A, B, dstate_p, chunks, d_flags, rec.get(),
+                                                         dcount_p);
   CSB_LAUNCH_CHECK();
-  std::vector<unsigned long long> hc(2 * n);
-  CSB_CUDA(cudaMemcpyAsync(state, dstate.get(), 2 * n * 8, cudaMemcpyDeviceToHost, st));
-  CSB_CUDA(cudaMemcpyAsync(hc.data(), dcount.get(), 2 * n * 8, cudaMemcpyDeviceToHost, st));
+  // state and counts are adjacent: one D2H into the pinned block (the host
+  // copies of c / h there are no longer needed)
+  CSB_CUDA(cudaMemcpyAsync(hp, dstate_p, 4 * n * 8, cudaMemcpyDeviceToHost, st));
   CSB_CUDA(cudaStreamSynchronize(st));
-  if (counts)
+  std::memcpy(state, hp, 2 * n * 8);
+  if (counts) {
+    const unsigned long long* hc = reinterpret_cast<const unsigned long long*>(hp + 2 * n);
     for (int64_t i = 0; i < 2 * n; ++i) counts[i] = static_cast<int64_t>(hc[i]);
+  }
 }
 
 // eigen_spectrum of a model trained on the certified-Cholesky path: re-form
@@ -1377,6 +1400,7 @@ cs_status cs_ctx_destroy(cs_ctx* ctx) {
     if (ctx->blas) cublas_api().destroy(ctx->blas);
     for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1], ctx->aux[2]})
       if (s) cudaStreamDestroy(s);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     delete ctx;
   });
 }

@@ -210,11 +210,14 @@ __device__ __forceinline__ void tag_wait_slots(Addr addr, unsigned tag, double (
     const ulonglong2* p = addr(u);
     r[u] = p ? tag_load(p) : make_ulonglong2(t, t);
   }
-  while (true) {
+  // bounded spin: a producer that can never arrive (a bug, or a co-residency
+  // violation) ends the kernel with an error instead of hanging the device
+  for (uint32_t spins = 0;; ++spins) {
     bool ok = true;
 #pragma unroll
     for (int u = 0; u < N; ++u) ok &= tag_ok(r[u], tag);
     if (ok) break;
+    if (spins > (1u << 24)) __trap();  // ~10 s of polling
 #pragma unroll
     for (int u = 0; u < N; ++u)
       if (!tag_ok(r[u], tag)) r[u] = tag_load(addr(u));

@@ -81,8 +81,11 @@ struct cs_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
-  static constexpr int kSlots = 3;  // host-API pipeline depth (streams / buffer sets)
-  cudaStream_t aux[kSlots] = {nullptr, nullptr, nullptr};
+#ifndef CSB_IO_SLOTS
+#define CSB_IO_SLOTS 3
+#endif
+  static constexpr int kSlots = CSB_IO_SLOTS;  // host-API pipeline depth (streams / buffer sets)
+  cudaStream_t aux[kSlots] = {};
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   int sm_count = 148;
@@ -1398,7 +1401,8 @@ cs_status cs_ctx_destroy(cs_ctx* ctx) {
     cudaDeviceSynchronize();  // workspaces are returned to the pool below
     if (ctx->solver) cusolver_api().destroy(ctx->solver);
     if (ctx->blas) cublas_api().destroy(ctx->blas);
-    for (auto s : {ctx->own, ctx->aux[0], ctx->aux[1], ctx->aux[2]})
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    for (auto s : ctx->aux)
       if (s) cudaStreamDestroy(s);
     if (ctx->pin) cudaFreeHost(ctx->pin);
     delete ctx;

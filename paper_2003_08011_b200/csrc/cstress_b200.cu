@@ -335,39 +335,29 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   return bisect_eigvals(st, d.get(), e.get(), m, w);
 }
 
-// eigenvalues (ascending) of the device tridiagonal (d, e) by bisection
+// eigenvalues (ascending) of the device tridiagonal (d, e) by bisection; the
+// Gershgorin interval and LAPACK dstebz's pivmin are reduced on the device
+// (no host round trip)
 bool bisect_eigvals(cudaStream_t st, const double* dd, const double* de, int64_t m, double* w) {
-  // Gershgorin interval of T (host: 2m doubles), LAPACK dstebz's pivmin
-  std::vector<double> hd(m), he(m + 1, 0.0);
-  CSB_CUDA(cudaMemcpyAsync(hd.data(), dd, m * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (m > 1) CSB_CUDA(cudaMemcpyAsync(he.data(), de, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CSB_CUDA(cudaStreamSynchronize(st));
-  double lo = 0.0, hi = 0.0, tnorm = 0.0, e2max = 0.0;
-  for (int64_t i = 0; i < m; ++i) {
-    const double r = (i > 0 ? std::fabs(he[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(he[i]) : 0.0);
-    lo = i == 0 ? hd[i] - r : std::min(lo, hd[i] - r);
-    hi = i == 0 ? hd[i] + r : std::max(hi, hd[i] + r);
-    if (i + 1 < m) e2max = std::max(e2max, he[i] * he[i]);
-  }
-  tnorm = std::max(std::fabs(lo), std::fabs(hi));
-  const double pivmin = 2.2250738585072014e-308 * std::max(1.0, e2max);
-  const double pad = 2.0 * 2.220446049250313e-16 * tnorm * static_cast<double>(m) + 2.0 * pivmin;
-  lo -= pad;
-  hi += pad;
-  const size_t smem = static_cast<size_t>(2) * m * sizeof(double);
-  tridiag_bisect_kernel<<<ceil_div(m, kBisectWarps), 128, smem, st>>>(dd, de, static_cast<int>(m), lo, hi, pivmin,
-                                                                       w);
+  TmpBuf<double> prm(3);
+  gershgorin_kernel<<<1, 1024, 0, st>>>(dd, de, static_cast<int>(m), prm.get());
   CSB_LAUNCH_CHECK();
-  CSB_CUDA(cudaStreamSynchronize(st));  // the temporaries go back to the pool
-  return true;
+  const size_t smem = static_cast<size_t>(2) * m * sizeof(double);
+  tridiag_bisect_kernel<<<ceil_div(m, kBisectWarps), 128, smem, st>>>(dd, de, static_cast<int>(m), prm.get(), w);
+  CSB_LAUNCH_CHECK();
+  return true;  // stream-ordered: the temporaries are freed on st after the kernels
 }
 
 // ---------------------------------------------------------- eigensolver
 // symmetric_eig (mset.cpp:57-70): precondition check, then cuSOLVER syevd
 // (FP64, ascending eigenvalues, orthonormal eigenvectors) in place on V.
-void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V, bool vectors = true) {
+// `check` = false for the train's own Gram matrices (mirrored, symmetric by
+// construction): skips the precondition's device reduction and host sync.
+void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V, bool vectors = true,
+                bool check = true) {
   cudaStream_t st = ctx->stream;
   if (m == 0) return;
+  if (check) {
   TmpBuf<unsigned long long> stats(2);
   CSB_CUDA(cudaMemsetAsync(stats.get(), 0, 2 * sizeof(unsigned long long), st));
   symmetry_stats_kernel<<<grid_for(m * m), 256, 0, st>>>(G, m, stats.get());
@@ -379,6 +369,7 @@ void eig_device(cs_ctx* ctx, const double* G, int64_t m, double* w, double* V, b
   std::memcpy(&mag, &hs[0], 8);
   std::memcpy(&asym, &hs[1], 8);
   if (asym > 1e-9 * std::max(mag, 1.0)) fail(CS_SHAPE_ERROR, "symmetric_eig: matrix is not symmetric to 1e-9");
+  }
   // eigenvalues only: own tridiagonalisation + bisection (m <= 2048)
   if (!vectors && tridiag_eigvals(ctx, G, m, w)) return;
   if (V != G) CSB_CUDA(cudaMemcpyAsync(V, G, m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -899,7 +890,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   if (!done) {
     // eigenvalues first: they decide the rank exactly as the reference does
     V.resize(m * m);
-    eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), vec_path);
+    eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), vec_path, false);
     trace.mark(vec_path ? "symmetric_eig (syevd)" : "eigenvalues (syevd N)");
     CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
                              cudaMemcpyDeviceToHost, st));
@@ -916,7 +907,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->rank = rank;
   if (!done) {
     if (!vec_path) {
-      eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), true);
+      eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), true, false);
       trace.mark("symmetric_eig (syevd V)");
       CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
                                cudaMemcpyDeviceToHost, st));
@@ -1353,7 +1344,7 @@ void materialize_spectrum(const cs_model* M) {
   TmpBuf<double> gram(m * m), V(m * m);
   form_gram(ctx, M, gram.get());
   M->spectrum.resize(m);
-  eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), false);
+  eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), false, false);
   CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
                            cudaMemcpyDeviceToHost, ctx->stream));
   CSB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -504,11 +504,52 @@ __device__ __forceinline__ double sturm_rcp(double q) {
   return r;
 }
 
+// Gershgorin interval of T widened by dstebz's pad, and its pivmin:
+// prm = {lo, hi, pivmin} (min / max reductions: order-independent)
+__global__ void __launch_bounds__(1024) gershgorin_kernel(const double* __restrict__ d,
+                                                          const double* __restrict__ e, int m,
+                                                          double* __restrict__ prm) {
+  __shared__ double slo[32], shi[32], se2[32];
+  double lo = INFINITY, hi = -INFINITY, e2 = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double r = __dadd_rn(i > 0 ? fabs(e[i - 1]) : 0.0, i + 1 < m ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, __dsub_rn(d[i], r));
+    hi = fmax(hi, __dadd_rn(d[i], r));
+    if (i + 1 < m) e2 = fmax(e2, __dmul_rn(e[i], e[i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    e2 = fmax(e2, __shfl_xor_sync(0xffffffffu, e2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    slo[threadIdx.x >> 5] = lo;
+    shi[threadIdx.x >> 5] = hi;
+    se2[threadIdx.x >> 5] = e2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < static_cast<int>(blockDim.x >> 5); ++q) {
+      lo = fmin(lo, slo[q]);
+      hi = fmax(hi, shi[q]);
+      e2 = fmax(e2, se2[q]);
+    }
+    const double tnorm = fmax(fabs(lo), fabs(hi));
+    const double pivmin = __dmul_rn(2.2250738585072014e-308, fmax(1.0, e2));
+    const double pad = __dadd_rn(__dmul_rn(__dmul_rn(2.0 * 2.220446049250313e-16, tnorm), static_cast<double>(m)),
+                                 __dmul_rn(2.0, pivmin));
+    prm[0] = __dsub_rn(lo, pad);
+    prm[1] = __dadd_rn(hi, pad);
+    prm[2] = pivmin;
+  }
+}
+
 constexpr int kBisectWarps = 4;  // eigenvalues per 128-thread block
 __global__ void __launch_bounds__(128) tridiag_bisect_kernel(const double* __restrict__ d,
                                                              const double* __restrict__ e, int m,
-                                                             double lo0, double hi0, double pivmin,
+                                                             const double* __restrict__ prm,
                                                              double* __restrict__ w) {
+  const double lo0 = prm[0], hi0 = prm[1], pivmin = prm[2];
   extern __shared__ double sh[];  // d [m], e^2 [m]
   double* sd = sh;
   double* se2 = sh + m;

@@ -181,8 +181,10 @@ double resolve_h(double h, int64_t n) {
 
 // --------------------------------------------------------------- selection
 // select_memory_vectors (mset.cpp:72-137); X is device N x n col-major.
+// picked_host == nullptr: the indices go to ctx's pinned block without a
+// sync (train_device copies them out after its final synchronisation)
 void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m,
-                   DevBuf<int64_t>& picked, std::vector<int64_t>& picked_host) {
+                   DevBuf<int64_t>& picked, std::vector<int64_t>* picked_host) {
   cudaStream_t st = ctx->stream;
   if (m < 2 * n) {
     char buf[160];
@@ -243,8 +245,13 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
                                            r1.get(), r2.get(), static_cast<int>(N), 0, 64, st));
   stride_pick_kernel<<<grid_for(m), 256, 0, st>>>(r2.get(), N, m, npicked.get(), picked.get());
   CSB_LAUNCH_CHECK();
-  picked_host.resize(m);
-  CSB_CUDA(cudaMemcpyAsync(picked_host.data(), picked.get(), m * sizeof(int64_t),
+  if (!picked_host) {
+    CSB_CUDA(cudaMemcpyAsync(ctx->pinned(m * sizeof(int64_t)), picked.get(), m * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+    return;
+  }
+  picked_host->resize(m);
+  CSB_CUDA(cudaMemcpyAsync(picked_host->data(), picked.get(), m * sizeof(int64_t),
                            cudaMemcpyDeviceToHost, st));
   CSB_CUDA(cudaStreamSynchronize(st));
 }
@@ -794,7 +801,6 @@ void pack_fp32_operands(cs_ctx* ctx, cs_model* M) {
         P.get(), M->p_shift.get(), n, m, M->bnB, M->ntB, M->kcB, M->p_gemm.get());
     CSB_LAUNCH_CHECK();
   }
-  CSB_CUDA(cudaStreamSynchronize(st));  // P is freed on return
 }
 
 // ----------------------------------------------------------------- train
@@ -834,7 +840,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->precision = precision;
   TmpBuf<int64_t> picked;
   trace.mark("enter");
-  select_device(ctx, X, N, n, m, picked, M->source_indices);  // mset.cpp:142
+  select_device(ctx, X, N, n, m, picked, nullptr);  // mset.cpp:142 (indices land in ctx->pin)
   trace.mark("select_memory_vectors");
   M->h = resolve_h(bandwidth, n);                            // mset.cpp:143-144
   M->D.resize(n * m);
@@ -928,6 +934,8 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
   CSB_CUDA(cudaStreamSynchronize(st));
   trace.mark("fp32 operand packing");
+  M->source_indices.resize(m);  // copied into ctx->pin by select_device, complete now
+  std::memcpy(M->source_indices.data(), ctx->pin, m * sizeof(int64_t));
   return M.release();
 }
 
@@ -1509,7 +1517,7 @@ cs_status cs_select_memory_vectors(cs_ctx* ctx, const double* X, int64_t N, int6
     CSB_CUDA(cudaMemcpyAsync(dX.get(), X, N * n * sizeof(double), cudaMemcpyHostToDevice, st));
     TmpBuf<int64_t> picked;
     std::vector<int64_t> host;
-    select_device(ctx, dX.get(), N, n, m, picked, host);
+    select_device(ctx, dX.get(), N, n, m, picked, &host);
     std::memcpy(idx, host.data(), m * sizeof(int64_t));
     if (D) {
       TmpBuf<double> dD(n * m);

@@ -897,7 +897,7 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
     // eigenvalues first: they decide the rank exactly as the reference does
     V.resize(m * m);
     eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), vec_path, false);
-    trace.mark(vec_path ? "symmetric_eig (syevd)" : "eigenvalues (syevd N)");
+    trace.mark(vec_path ? "symmetric_eig (syevd)" : "eigenvalues (own solver up to m = 2048, syevd N above)");
     CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
                              cudaMemcpyDeviceToHost, st));
     CSB_CUDA(cudaStreamSynchronize(st));

@@ -9,8 +9,10 @@ Same outputs, messages and exit codes as the reference's ``cmd_sweep`` /
 ``cmd_speedup``: cost_train.csv, cost_surveil.csv, surface.json (sweep),
 speedup_train.csv, speedup_surveil.csv (speedup) and a manifest.json in
 the output directory; exit 0 success, 2 configuration error, 4 empty grid,
-5 runtime failure after partial output (the cells completed so far are
-written with ``metadata.partial = true``, main.cpp:205-231).  The
+5 runtime failure after partial output (main.cpp:205-231: the cells
+reported so far are written with ``metadata.partial = true``; the records
+of a multi-rank sweep only reach rank 0 at the final gather, so a failure
+before it leaves an empty partial surface).  The
 reference's ``synth`` command (signal files, moment reports) is outside
 this library's scope.
 """

@@ -871,7 +871,37 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
   M->pinv.resize(m * m);
   bool done = false;
   int64_t rank = 0;
-  if (!vec_path && !eager && cholesky_inverse(ctx, gram.get(), m, M->pinv.get())) {
+  // Eager spectrum with the own eigenvalue solver (m <= kTriMaxM, no host
+  // round trip inside): it runs on a side stream concurrently with the
+  // certified Cholesky inverse, which decides rank == m on its own; the
+  // spectrum is joined before train returns (the reference's contract,
+  // mset.cpp:153-154).  If the certification fails, the eigenvalues decide
+  // the rank as below.
+  const bool eig_async = eager && !vec_path && m <= kTriMaxM;
+  TmpBuf<double> V;  // syevd works in place on a copy of G
+  cudaEvent_t eig_done = nullptr;
+  if (eig_async) {
+    V.resize(m * m);  // only touched if the own solver falls back to syevd
+    cudaStream_t side = ctx->aux[0];
+    cudaEvent_t gram_ready;
+    CSB_CUDA(cudaEventCreateWithFlags(&gram_ready, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&eig_done, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventRecord(gram_ready, st));
+    CSB_CUDA(cudaStreamWaitEvent(side, gram_ready, 0));
+    cudaEventDestroy(gram_ready);
+    {
+      struct Swap {  // ctx->stream is the side stream for this call only
+        cs_ctx* c;
+        cudaStream_t keep;
+        ~Swap() { c->stream = keep; }
+      } swap{ctx, st};
+      ctx->stream = side;
+      StreamScope scope(side);
+      eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), false, false);
+    }
+    CSB_CUDA(cudaEventRecord(eig_done, side));
+  }
+  if (!vec_path && (!eager || eig_async) && cholesky_inverse(ctx, gram.get(), m, M->pinv.get())) {
     TmpBuf<unsigned long long> nrm(2);
     CSB_CUDA(cudaMemsetAsync(nrm.get(), 0, 2 * sizeof(unsigned long long), st));
     const int nb = static_cast<int>(std::min<int64_t>(m, 4 * 148));
@@ -888,15 +918,19 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
     if (std::isfinite(g1 * gi1) && g1 * gi1 < kCertifiedCond) {
       rank = m;
       done = true;
-      M->spectrum_ready = false;
+      M->spectrum_ready = eig_async;  // eager: computed beside, joined below
     }
     trace.mark("pinv (certified Cholesky)");
   }
-  TmpBuf<double> V;  // syevd works in place on a copy of G
+  if (eig_async && !done) {  // the eigenvalues decide the rank: join now
+    CSB_CUDA(cudaStreamWaitEvent(st, eig_done, 0));
+    cudaEventDestroy(eig_done);
+    eig_done = nullptr;
+  }
   if (!done) {
     // eigenvalues first: they decide the rank exactly as the reference does
     V.resize(m * m);
-    eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), vec_path, false);
+    if (!eig_async) eig_device(ctx, gram.get(), m, M->spectrum.get(), V.get(), vec_path, false);
     trace.mark(vec_path ? "symmetric_eig (syevd)" : "eigenvalues (own solver up to m = 2048, syevd N above)");
     CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
                              cudaMemcpyDeviceToHost, st));
@@ -932,6 +966,12 @@ cs_model* train_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64
     trace.mark("pinv (W W^T)");
   }
   if (precision == CS_PRECISION_FP32) pack_fp32_operands(ctx, M.get());
+  if (eig_done) {  // certified while the spectrum was computed beside: join it last
+    CSB_CUDA(cudaStreamWaitEvent(st, eig_done, 0));
+    cudaEventDestroy(eig_done);
+    CSB_CUDA(cudaMemcpyAsync(M->spectrum_host.data(), M->spectrum.get(), m * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+  }
   CSB_CUDA(cudaStreamSynchronize(st));
   trace.mark("fp32 operand packing");
   M->source_indices.resize(m);  // copied into ctx->pin by select_device, complete now

@@ -316,7 +316,15 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   CSB_CUDA(cudaMemsetAsync(kb.get(), 0, 2 * static_cast<size_t>(P) * sizeof(ulonglong2), st));
   const bool trace = std::getenv("CSB_EIG_TRACE") != nullptr;  // development: per-step timeline
   TmpBuf<unsigned long long> tr(trace ? 4 * m : 1);
-  TriGridArgs ga{G, static_cast<int>(m), P, d.get(), e.get(), pb.get(), rb.get(), kb.get(), trace ? tr.get() : nullptr};
+  // the last kTriCtaMaxM columns go to the one-CTA kernel (~2 us per step
+  // there against ~6.5 us per grid step: the exchange latency)
+  // (measured: -7..-10% at m = 500 .. 2000; at m <= 2 kTriCtaMaxM the grid
+  // part is too short to pay for the hand-off)
+  const int nt = (std::getenv("CSB_EIG_NO_TAIL") || m <= 2 * kTriCtaMaxM) ? 2 : kTriCtaMaxM;
+  const int kstop = static_cast<int>(m) - nt;
+  TmpBuf<double> tail(static_cast<size_t>(nt) * nt);
+  TriGridArgs ga{G, static_cast<int>(m), P, d.get(), e.get(), pb.get(), rb.get(), kb.get(), trace ? tr.get() : nullptr,
+                 kstop, tail.get()};
   void* args[] = {&ga};
   const cudaError_t launched = cudaLaunchCooperativeKernel(fn, dim3(P), dim3(kTriGridThreads), args, smem, st);
   if (launched == cudaErrorCooperativeLaunchTooLarge || launched == cudaErrorNotSupported) {
@@ -331,13 +339,24 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
     CSB_CUDA(cudaStreamSynchronize(st));
     double s3[3] = {0, 0, 0};
     int cnt = 0;
-    for (int64_t k = 0; k + 3 < m; ++k, ++cnt) {
+    for (int64_t k = 0; k + 1 < kstop; ++k, ++cnt) {
       s3[0] += double(h[4 * k + 2] - h[4 * k + 1]);        // exchange (slowest CTA + hop)
       s3[1] += double(h[4 * k + 3] - h[4 * k + 2]);        // update + next reflector
       s3[2] += double(h[4 * (k + 1) + 1] - h[4 * k + 3]);  // row sums + publish
     }
     std::fprintf(stderr, "eig grid m=%lld P=%d ns/step: exchange %.0f  update+reflector %.0f  row sums %.0f\n",
                  static_cast<long long>(m), P, s3[0] / cnt, s3[1] / cnt, s3[2] / cnt);
+  }
+  if (nt > 2) {
+    // (the attribute is per (function, device): set by the small path above on first use)
+    static std::atomic<unsigned long long> tail_attr_dev{0};
+    if (!(tail_attr_dev.load() >> ctx->device & 1ull)) {
+      CSB_CUDA(cudaFuncSetAttribute(tridiag_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(tri_cta_smem(kTriCtaMaxM))));
+      tail_attr_dev.fetch_or(1ull << ctx->device);
+    }
+    tridiag_cta_kernel<<<1, kTriCtaThreads, tri_cta_smem(nt), st>>>(tail.get(), nt, d.get() + kstop, e.get() + kstop);
+    CSB_LAUNCH_CHECK();
   }
   return bisect_eigvals(st, d.get(), e.get(), m, w);
 }

@@ -134,7 +134,10 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
 }
 
 // Larger matrices (kTriCtaMaxM < m <= kTriMaxM): the same reduction by a
-// co-resident grid (cooperative launch, one CTA per SM) with the whole
+// co-resident grid for all but the last kTriCtaMaxM columns (m > 2
+// kTriCtaMaxM), whose trailing block the one-CTA kernel finishes (its steps
+// cost ~2 us against the grid's ~6.5 us exchange-bound ones).  The grid is a
+// co-resident one (cooperative launch, one CTA per SM) with the whole
 // matrix in SHARED memory -- CTA c keeps the full rows i = c, c + P, ...
 // (cyclic, so the shrinking trailing block stays balanced; at most
 // kTriGridRows rows of m doubles); thread t owns the columns j = t + u T.
@@ -174,6 +177,8 @@ struct TriGridArgs {
   ulonglong2* rbuf;  // [2][m] tagged row k + 2
   ulonglong2* kbuf;  // [2][P] tagged partials of p^T v
   unsigned long long* trace;  // development: [m][4] globaltimer stamps of CTA 0, or nullptr
+  int kstop;                  // steps 0 .. kstop - 1 here (kstop <= m - 2) ...
+  double* tail;               // ... then rows / cols >= kstop go here (column-major, m - kstop square)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -316,7 +321,8 @@ __global__ void __launch_bounds__(kTriGridThreads, 1) tridiag_grid_kernel(TriGri
   double tau;
   reflector(0, vr, tau);
 
-  for (int k = 0; k + 2 < m; ++k) {
+  const int kstop = a.kstop;
+  for (int k = 0; k < kstop; ++k) {
     const unsigned tag = static_cast<unsigned>(k + 1);
     const int par = k & 1;
     ulonglong2* pb = a.pbuf + static_cast<size_t>(par) * m;
@@ -464,13 +470,13 @@ __global__ void __launch_bounds__(kTriGridThreads, 1) tridiag_grid_kernel(TriGri
         }
       }
     }
-    if (k + 3 < m) {
+    if (k + 1 < kstop) {
       publish_row(k + 1);
       // the next reflector from row k + 1, which is final now
 #pragma unroll
       for (int u = 0; u < NC; ++u) vr[u] = r1[u];
       reflector(k + 1, vr, tau);
-    } else {
+    } else if (kstop == m - 2) {
       // the last 2 x 2 block: rows m - 2 (= k + 1) and m - 1 (= k + 2)
 #pragma unroll
       for (int u = 0; u < NC; ++u) {
@@ -485,6 +491,20 @@ __global__ void __launch_bounds__(kTriGridThreads, 1) tridiag_grid_kernel(TriGri
 #pragma unroll
     for (int u = 0; u < NC; ++u) r1[u] = r2[u];
     if (a.trace && c == 0 && tid == 0) a.trace[4 * k + 3] = gtimer();
+  }
+  if (kstop < m - 2) {
+    // hand the trailing block (as updated by step kstop - 1) to the one-CTA
+    // kernel: each thread its own columns of the owned rows i >= kstop
+    const int nt = m - kstop;
+    for (int r = 0; r < R; ++r) {
+      const int i = c + r * P;
+      if (i < kstop) continue;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int j = tid + u * T;
+        if (j >= kstop && j < m) a.tail[static_cast<size_t>(j - kstop) * nt + (i - kstop)] = At[r * LD + u * T];
+      }
+    }
   }
 }
 

@@ -36,7 +36,8 @@ def _err(w, want):
     return float(np.abs(np.asarray(w) - want).max() / max(np.abs(want).max(), 1e-300))
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 5, 17, 33, 100, 127, 129, 161, 256, 257, 513, 1000, 1025, 2047, 2048])
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 17, 33, 100, 127, 129, 161, 256, 257, 320, 321, 513, 1000, 1025, 2047,
+                               2048])
 def test_random_symmetric(p, m):
     rng = np.random.default_rng(m)
     A = rng.standard_normal((m, m))
@@ -125,6 +126,21 @@ def test_already_reduced_columns(p, kind):
     want = np.linalg.eigvalsh(A)
     w = p.symmetric_eigvals(A)
     assert float(np.abs(w - want).max()) <= 1e-12 * max(np.abs(want).max(), 1.0)
+
+
+@pytest.mark.parametrize("m", [321, 700])
+def test_grid_then_one_cta_tail(p, monkeypatch, m):
+    """Above m = 320 the grid reduces all but the last 160 columns and the
+    one-CTA kernel finishes the trailing block; the same numbers (to
+    rounding) as the grid alone (CSB_EIG_NO_TAIL=1)."""
+    rng = np.random.default_rng(m)
+    A = rng.standard_normal((m, m))
+    A = np.asfortranarray(A @ A.T)
+    want = np.linalg.eigvalsh(A)
+    tail = p.symmetric_eigvals(A)
+    monkeypatch.setenv("CSB_EIG_NO_TAIL", "1")
+    grid = p.symmetric_eigvals(A)
+    assert _err(tail, want) <= 1e-12 and _err(grid, want) <= 1e-12 and _err(tail, grid) <= 1e-12
 
 
 def test_above_own_range_uses_syevd(p):

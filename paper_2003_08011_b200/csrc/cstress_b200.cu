@@ -261,6 +261,59 @@ void select_device(cs_ctx* ctx, const double* X, int64_t N, int64_t n, int64_t m
 // Returns false when the grid cannot be co-resident (the caller then uses
 // syevd).  w is a device array (ascending).
 bool bisect_eigvals(cudaStream_t st, const double* dd, const double* de, int64_t m, double* w);
+// one 16-CTA cluster reduces the m x m block G (m <= kTriClusterMaxM) to
+// (d, e); false when the device cannot launch such a cluster
+bool tri_cluster_available(cs_ctx* ctx) {
+  if (std::getenv("CSB_EIG_NO_CLUSTER")) return false;
+  static int ok_by_dev[64] = {};  // 0 unknown, 1 yes, -1 no
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    int& ok = ok_by_dev[ctx->device & 63];
+    if (ok == 0) {
+      ok = -1;
+      if (cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+              cudaSuccess &&
+          cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(tri_cluster_smem())) == cudaSuccess) {
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(kTriClusterSize);
+        q.blockDim = dim3(kTriGridThreads);
+        q.dynamicSmemBytes = tri_cluster_smem();
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = kTriClusterSize;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        q.attrs = &at;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, tridiag_cluster_kernel, &q) == cudaSuccess && n > 0) ok = 1;
+      }
+      cudaGetLastError();
+    }
+    return ok == 1;
+  }
+}
+bool tri_cluster_reduce(cs_ctx* ctx, cudaStream_t st, const double* G, int64_t m, double* d, double* e) {
+  if (m > kTriClusterMaxM || !tri_cluster_available(ctx)) return false;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kTriClusterSize);
+  cfg.blockDim = dim3(kTriGridThreads);
+  cfg.dynamicSmemBytes = tri_cluster_smem();
+  cfg.stream = st;
+  cudaLaunchAttribute at{};
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = kTriClusterSize;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  CSB_CUDA(cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, G, static_cast<int>(m), d, e));
+  CSB_LAUNCH_CHECK();
+  return true;
+}
+
 bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   if (m < 1 || m > kTriMaxM) return false;
   // Default for m <= kTriMaxM, where it beats syevd: one CTA with the matrix
@@ -284,6 +337,8 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
     CSB_LAUNCH_CHECK();
     return bisect_eigvals(st, d.get(), e.get(), m, w);
   }
+  // one 16-CTA cluster with the whole matrix in distributed shared memory
+  if (tri_cluster_reduce(ctx, st, G, m, d.get(), e.get())) return bisect_eigvals(st, d.get(), e.get(), m, w);
   // co-resident grid, rows in shared memory: up to kTriGridRows rows of
   // NC x kTriGridThreads doubles per CTA, as many CTAs as that takes (<= SMs)
   int sms = 0, optin = 0;
@@ -320,7 +375,11 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   // there against ~6.5 us per grid step: the exchange latency)
   // (measured: -7..-10% at m = 500 .. 2000; at m <= 2 kTriCtaMaxM the grid
   // part is too short to pay for the hand-off)
-  const int nt = (std::getenv("CSB_EIG_NO_TAIL") || m <= 2 * kTriCtaMaxM) ? 2 : kTriCtaMaxM;
+  const bool cl_tail = m > kTriClusterMaxM + 2 && tri_cluster_available(ctx);
+  const int nt = std::getenv("CSB_EIG_NO_TAIL") ? 2
+                 : cl_tail                       ? kTriClusterMaxM
+                 : (m <= 2 * kTriCtaMaxM)        ? 2
+                                                 : kTriCtaMaxM;
   const int kstop = static_cast<int>(m) - nt;
   TmpBuf<double> tail(static_cast<size_t>(nt) * nt);
   TriGridArgs ga{G, static_cast<int>(m), P, d.get(), e.get(), pb.get(), rb.get(), kb.get(), trace ? tr.get() : nullptr,
@@ -347,7 +406,10 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
     std::fprintf(stderr, "eig grid m=%lld P=%d ns/step: exchange %.0f  update+reflector %.0f  row sums %.0f\n",
                  static_cast<long long>(m), P, s3[0] / cnt, s3[1] / cnt, s3[2] / cnt);
   }
-  if (nt > 2) {
+  if (nt == kTriClusterMaxM) {
+    if (!tri_cluster_reduce(ctx, st, tail.get(), nt, d.get() + kstop, e.get() + kstop))
+      fail(CS_ERROR, "eigenvalues: cluster tail launch failed");
+  } else if (nt > 2) {
     // (the attribute is per (function, device): set by the small path above on first use)
     static std::atomic<unsigned long long> tail_attr_dev{0};
     if (!(tail_attr_dev.load() >> ctx->device & 1ull)) {

@@ -24,9 +24,12 @@
 // to the last bit (one warp per eigenvalue, 32 shifts per round).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace csb {
+namespace cg = cooperative_groups;
 
 constexpr int kTriMaxM = 2048;
 constexpr int kTriCtaMaxM = 160;
@@ -133,9 +136,10 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
   }
 }
 
-// Larger matrices (kTriCtaMaxM < m <= kTriMaxM): the same reduction by a
-// co-resident grid for all but the last kTriCtaMaxM columns (m > 2
-// kTriCtaMaxM), whose trailing block the one-CTA kernel finishes (its steps
+// Larger matrices (kTriClusterMaxM < m <= kTriMaxM): the same reduction by a
+// co-resident grid for all but the last kTriClusterMaxM columns, whose
+// trailing block the 16-CTA cluster kernel below finishes (or, without
+// clusters, all but the last kTriCtaMaxM for the one-CTA kernel: its steps
 // cost ~2 us against the grid's ~6.5 us exchange-bound ones).  The grid is a
 // co-resident one (cooperative launch, one CTA per SM) with the whole
 // matrix in SHARED memory -- CTA c keeps the full rows i = c, c + P, ...
@@ -506,6 +510,240 @@ __global__ void __launch_bounds__(kTriGridThreads, 1) tridiag_grid_kernel(TriGri
       }
     }
   }
+}
+
+// Trailing blocks up to kTriClusterMaxM (and whole matrices of that size):
+// the same one-exchange-per-step reduction by ONE 16-CTA cluster, the
+// exchange through distributed shared memory and one cluster barrier per
+// step instead of tagged L2 words (a cluster barrier plus DSMEM reads cost
+// well under the ~2.5 us L2 round trip of the grid).  CTA c keeps rows
+// i = c, c + 16, ... (at most kTriClusterRows) of the block in shared memory.
+// Per step: the owned rows' p_i and the CTA's partial of p^T v go to this
+// CTA's shared memory (by step parity); cluster barrier; every CTA reads the
+// p_j of its columns, row k + 2 (published by its owner at the end of the
+// previous step) and the 16 partials from the other CTAs' shared memory.  A
+// CTA can run at most one step ahead (the barrier), so two generations of
+// every buffer suffice.
+constexpr int kTriClusterSize = 16;
+constexpr int kTriClusterRows = 32;
+constexpr int kTriClusterNC = 2;  // column slots per thread (256 threads)
+constexpr int kTriClusterMaxM = kTriClusterNC * kTriGridThreads;  // 512
+constexpr int kTriClusterSmall = 2 * kTriClusterRows /*pbuf*/ + 2 /*kpart*/ + 2 * kTriClusterRows /*vo, po*/ +
+                                 kTriClusterRows * (kTriGridThreads / 32) /*red*/ + kTriGridThreads / 32 + 8;
+__host__ __device__ constexpr size_t tri_cluster_smem() {
+  return sizeof(double) * (static_cast<size_t>(kTriClusterRows + 2) * kTriClusterMaxM + kTriClusterSmall);
+}
+
+__global__ void __launch_bounds__(kTriGridThreads, 1) tridiag_cluster_kernel(const double* __restrict__ G, int m,
+                                                                             double* __restrict__ dout,
+                                                                             double* __restrict__ eout) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double sm[];
+  constexpr int T = kTriGridThreads, NW = T / 32, NC = kTriClusterNC, LD = NC * T, P = kTriClusterSize;
+  const int c = static_cast<int>(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = (m - c + P - 1) / P;  // rows i = c + r P, r < R
+  double* pbuf = sm;                            // [2][kTriClusterRows] p of the owned rows (read remotely)
+  double* kpart = pbuf + 2 * kTriClusterRows;   // [2] this CTA's partial of p^T v (read remotely)
+  double* vo = kpart + 2;                       // [kTriClusterRows]
+  double* po = vo + kTriClusterRows;            // [kTriClusterRows]
+  double* red = po + kTriClusterRows;           // [kTriClusterRows][NW]
+  double* scratch = red + kTriClusterRows * NW;  // [NW]
+  double* bc = scratch + NW;
+  double* rowbuf = sm + kTriClusterSmall;       // [2][LD] row k + 2 by step parity (read remotely)
+  double* At = rowbuf + 2 * LD + tid;           // owned rows: (r, u) at r LD + u T
+  for (int r = 0; r < kTriClusterRows; ++r) {
+    const double* gcol = G + static_cast<size_t>(min(c + r * P, m - 1)) * m;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      At[r * LD + u * T] = r < R && j < m ? gcol[j] : 0.0;
+    }
+  }
+  if (tid < 2 * kTriClusterRows) vo[tid] = 0.0;  // vo, po
+  double r1[NC], vr[NC];
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int j = tid + u * T;
+    r1[u] = j < m ? G[static_cast<size_t>(1) * m + j] : 0.0;
+    vr[u] = j < m ? G[j] : 0.0;
+  }
+  auto reflector = [&](int kk, double (&x)[NC], double& tau_out) {
+    double sig = 0.0;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      if (j > kk + 1 && j < m) sig = fma(x[u], x[u], sig);
+      if (j == kk + 1) bc[0] = x[u];
+      if (j == kk && c == 0) dout[kk] = x[u];
+    }
+    for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
+    if (lane == 0) scratch[warp] = sig;
+    __syncthreads();
+    double S = 0.0;
+    for (int w = 0; w < NW; ++w) S += scratch[w];
+    const double al = bc[0];
+    double tau = 0.0, scal = 0.0, beta = al;
+    if (S > 0.0) {
+      const double nrm = sqrt(al * al + S);
+      beta = -copysign(nrm, al);
+      tau = (beta - al) / beta;
+      scal = 1.0 / (al - beta);
+    }
+    if (c == 0 && tid == 0) eout[kk] = beta;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      x[u] = j == kk + 1 ? 1.0 : (j > kk + 1 && j < m ? x[u] * scal : 0.0);
+    }
+    tau_out = tau;
+    __syncthreads();
+  };
+  // row kk + 2 as it stands after step kk - 1 into this CTA's rowbuf (kk & 1)
+  auto publish_row = [&](int kk) {
+    if ((kk + 2) % P == c) {
+      const double* row = At + ((kk + 2) / P) * LD;
+      double* rb = rowbuf + (kk & 1) * LD + tid;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) rb[u * T] = row[u * T];
+    }
+  };
+  __syncthreads();
+  if (m > 2) publish_row(0);
+  double tau;
+  reflector(0, vr, tau);
+  for (int k = 0; k + 2 < m; ++k) {
+    const int par = k & 1;
+    const int rlo = c > k ? 0 : (k - c) / P + 1;
+    bool live[NC];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) live[u] = u * T + warp * 32 + 31 > k && u * T + warp * 32 < m;
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      if (j > k && j < m && j % P == c) vo[j / P] = vr[u];
+    }
+    // row sums in two passes of 16 rows (transposing butterfly)
+#pragma unroll
+    for (int r0 = 0; r0 < kTriClusterRows; r0 += 16) {
+      double acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int r = r0 + q;
+        acc[q] = 0.0;
+        if (r >= rlo && r < R) {
+#pragma unroll
+          for (int u = 0; u < NC; ++u)
+            if (live[u]) acc[q] = fma(At[r * LD + u * T], vr[u], acc[q]);
+        }
+      }
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1) {
+        const bool up = lane & (2 * h);
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+          const double send = up ? acc[i] : acc[i + h];
+          const double keep = up ? acc[i + h] : acc[i];
+          acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+        }
+      }
+      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+      if ((lane & 1) == 0) red[(r0 + (lane >> 1)) * NW + warp] = acc[0];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int r = lane;  // kTriClusterRows == 32
+      double pv = 0.0;
+      if (r < rlo) vo[r] = po[r] = 0.0;
+      if (r >= rlo && r < R) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += red[r * NW + w];
+        const double pi = tau * s;
+        po[r] = pi;
+        pbuf[par * kTriClusterRows + r] = pi;
+        pv = pi * vo[r];
+      }
+      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+      if (lane == 0) kpart[par] = pv;
+    }
+    cluster.sync();  // every CTA's p, partial and row k + 2 are published
+    double pw[NC], r2[NC];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      pw[u] = 0.0;
+      r2[u] = 0.0;
+      if (j > k && j < m) {
+        const double* rp = cluster.map_shared_rank(pbuf, j % P);
+        pw[u] = rp[par * kTriClusterRows + j / P];
+      }
+      if (j >= k + 2 && j < m) {
+        const double* rr = cluster.map_shared_rank(rowbuf, (k + 2) % P);
+        r2[u] = rr[par * LD + j];
+      }
+    }
+    if (warp == 0) {
+      double K = lane < P ? cluster.map_shared_rank(kpart, lane)[par] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+      if (lane == 0) bc[3] = K;
+    }
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+      const int j = tid + u * T;
+      if (j == k + 1) bc[4] = pw[u];
+      if (j == k + 2) {
+        bc[5] = pw[u];
+        bc[6] = vr[u];
+      }
+    }
+    __syncthreads();
+    const double hk = 0.5 * tau * bc[3];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) pw[u] = pw[u] - hk * vr[u];
+#pragma unroll 4
+    for (int r = 0; r < kTriClusterRows; ++r) {
+      if (r >= rlo && r < R) {
+        const double vi = vo[r], wi = po[r] - hk * vi;
+        double x[NC];
+#pragma unroll
+        for (int u = 0; u < NC; ++u) x[u] = live[u] ? At[r * LD + u * T] : 0.0;
+#pragma unroll
+        for (int u = 0; u < NC; ++u)
+          if (live[u] && tid + u * T < m) At[r * LD + u * T] = x[u] - __dadd_rn(__dmul_rn(vi, pw[u]), __dmul_rn(wi, vr[u]));
+      }
+    }
+    {
+      const double w1 = bc[4] - hk * 1.0;
+      const double v2 = bc[6], w2 = bc[5] - hk * v2;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int j = tid + u * T;
+        if (j > k && j < m) {
+          r1[u] -= __dadd_rn(__dmul_rn(1.0, pw[u]), __dmul_rn(w1, vr[u]));
+          r2[u] -= __dadd_rn(__dmul_rn(v2, pw[u]), __dmul_rn(w2, vr[u]));
+        }
+      }
+    }
+    if (k + 3 < m) {
+      publish_row(k + 1);
+#pragma unroll
+      for (int u = 0; u < NC; ++u) vr[u] = r1[u];
+      reflector(k + 1, vr, tau);
+    } else {
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        const int j = tid + u * T;
+        if (c == 0 && j == m - 2) dout[m - 2] = r1[u];
+        if (c == 0 && j == m - 1) {
+          eout[m - 2] = r1[u];
+          dout[m - 1] = r2[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NC; ++u) r1[u] = r2[u];
+  }
+  cluster.sync();  // no CTA leaves while peers may still read its shared memory
 }
 
 // Eigenvalues of the symmetric tridiagonal (d, e), ascending: one WARP per

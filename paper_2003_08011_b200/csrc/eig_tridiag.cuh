@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
 // co-resident grid for all but the last kTriClusterMaxM columns, whose
 // trailing block the 16-CTA cluster kernel below finishes (or, without
 // clusters, all but the last kTriCtaMaxM for the one-CTA kernel: its steps
-// cost ~2 us against the grid's ~6.5 us exchange-bound ones).  The grid is a
+// cost ~4 us on a 160 block against the grid's ~6.5 us exchange-bound ones).  The grid is a
 // co-resident one (cooperative launch, one CTA per SM) with the whole
 // matrix in SHARED memory -- CTA c keeps the full rows i = c, c + P, ...
 // (cyclic, so the shrinking trailing block stays balanced; at most

@@ -371,7 +371,7 @@ bool tridiag_eigvals(cs_ctx* ctx, const double* G, int64_t m, double* w) {
   CSB_CUDA(cudaMemsetAsync(kb.get(), 0, 2 * static_cast<size_t>(P) * sizeof(ulonglong2), st));
   const bool trace = std::getenv("CSB_EIG_TRACE") != nullptr;  // development: per-step timeline
   TmpBuf<unsigned long long> tr(trace ? 4 * m : 1);
-  // the last kTriCtaMaxM columns go to the one-CTA kernel (~2 us per step
+  // the last kTriCtaMaxM columns go to the one-CTA kernel (~4 us per step
   // there against ~6.5 us per grid step: the exchange latency)
   // (measured: -7..-10% at m = 500 .. 2000; at m <= 2 kTriCtaMaxM the grid
   // part is too short to pay for the hand-off)

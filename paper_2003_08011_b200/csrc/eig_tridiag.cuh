@@ -54,7 +54,6 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
   double* w = p + m;
   double* part = w + m;  // [kTriCtaThreads] row partials by column phase
   double* scratch = part + kTriCtaThreads;
-  double* bc = scratch + kTriCtaThreads / 32;
   const int tid = threadIdx.x;
   for (int idx = tid; idx < m * m; idx += blockDim.x) {
     const int i = idx % m, j = idx / m;
@@ -78,23 +77,24 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
       sig += x * x;
     }
     sig = bsum(sig);
+    // every thread forms the reflector itself (the same values): no
+    // broadcast through shared memory and no barrier for it
+    const double al = A[i0 + k * ld];
+    double tau = 0.0, scal = 0.0, beta = al;
+    if (sig > 0.0) {
+      const double nrm = sqrt(al * al + sig);
+      beta = -copysign(nrm, al);
+      tau = (beta - al) / beta;
+      scal = 1.0 / (al - beta);
+    }
     if (tid == 0) {
-      const double al = A[i0 + k * ld];
-      double tau = 0.0, scal = 0.0, beta = al;
-      if (sig > 0.0) {
-        const double nrm = sqrt(al * al + sig);
-        beta = -copysign(nrm, al);
-        tau = (beta - al) / beta;
-        scal = 1.0 / (al - beta);
-      }
       d[k] = A[k + k * ld];
       e[k] = beta;
-      bc[0] = tau;
-      bc[1] = scal;
     }
-    __syncthreads();
-    const double tau = bc[0], scal = bc[1];
-    if (tau == 0.0) continue;  // uniform
+    if (tau == 0.0) {  // uniform
+      __syncthreads();  // bsum's scratch is reused next step
+      continue;
+    }
     for (int i = i0 + tid; i < m; i += blockDim.x) v[i] = i == i0 ? 1.0 : A[i + k * ld] * scal;
     __syncthreads();
     // p = tau A22 v: (row, column phase) per thread, phases summed in order
@@ -121,9 +121,12 @@ __global__ void __launch_bounds__(kTriCtaThreads, 1) tridiag_cta_kernel(const do
     const double K = bsum(pv);
     for (int i = i0 + tid; i < m; i += blockDim.x) w[i] = p[i] - 0.5 * tau * K * v[i];
     __syncthreads();
-    for (int idx = tid; idx < mp * mp; idx += blockDim.x) {
-      const int i = i0 + idx % mp, j = i0 + idx / mp;
-      A[i + j * ld] -= __dadd_rn(__dmul_rn(v[i], w[j]), __dmul_rn(w[i], v[j]));
+    // rank-2 update: a warp per column, lanes down the rows (no index
+    // division per element)
+    for (int j = i0 + (tid >> 5); j < m; j += kTriCtaThreads / 32) {
+      const double vj = v[j], wj = w[j];
+      for (int i = i0 + (tid & 31); i < m; i += 32)
+        A[i + j * ld] -= __dadd_rn(__dmul_rn(v[i], wj), __dmul_rn(w[i], vj));
     }
     __syncthreads();
   }

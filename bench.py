@@ -752,11 +752,22 @@ def run_b200(args, world, rank, local):
     clocks = sampler.stop()
     e2e_mean = max_over_ranks(statistics.mean(e2e_t))
 
+    # secondary sections: a failure is recorded in the line instead of losing
+    # the headline (the traceback goes to stderr)
+    def section(name, fn):
+        try:
+            return fn()
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+            traceback.print_exc(file=sys.stderr)
+            return {"error": f"{name}: {type(exc).__name__}: {exc}"}
+
     # ---- C5' (configs[4]): train once, broadcast, observation shards
-    c5 = None if args.no_c5 else run_c5(args, world, rank, local, barrier, max_over_ranks)
+    c5 = None if args.no_c5 else section("c5", lambda: run_c5(args, world, rank, local, barrier, max_over_ranks))
 
     # ---- Monte Carlo scoping sweep (cells/s), strong scaling over ranks
-    sweep = None if args.no_sweep else run_bench_sweep(world, rank, local, barrier, max_over_ranks)
+    sweep = None if args.no_sweep else section(
+        "sweep", lambda: run_bench_sweep(world, rank, local, barrier, max_over_ranks))
 
     if rank != 0:
         return
@@ -807,15 +818,15 @@ def run_b200(args, world, rank, local):
         line["c5"] = c5
     if world == 1:
         if not args.no_c1:
-            line["c1"] = run_c1(args, local, args.steps)
+            line["c1"] = section("c1", lambda: run_c1(args, local, args.steps))
         if not args.no_c3:
-            line["c3"] = run_c3(args, local)
+            line["c3"] = section("c3", lambda: run_c3(args, local))
         if not args.no_sprt:
-            line["sprt"] = run_sprt_bench(local)
+            line["sprt"] = section("sprt", lambda: run_sprt_bench(local))
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_c2(train, obs)
+            line["cpu_baseline"] = section("cpu_baseline", lambda: cpu_baseline_c2(train, obs))
             if not args.no_sweep:
-                line["host_sweep"] = run_host_sweep(local)
+                line["host_sweep"] = section("host_sweep", lambda: run_host_sweep(local))
     print(json.dumps(line), flush=True)
 
 
